@@ -1,0 +1,219 @@
+/*
+ * lockstep_b200.h — C ABI of the B200 program-counter VM.
+ *
+ * This is the drop-in boundary for the reference's execution engine,
+ * `lockstep.pc_vm` (reference pkg/src/lockstep/pc_vm.py). Each entry point
+ * names the reference interface it replaces:
+ *
+ *   ls_program_create / ls_program_bind_target
+ *       <- the CompiledProgram consumed by pc_vm.init_machine
+ *          (compiler.py:52-71, pc_vm.py:140-213) plus the target kernels
+ *          registered by workloads._make_target (workloads.py:158-171)
+ *   ls_machine_create / ls_machine_set_input
+ *       <- pc_vm.init_machine (pc_vm.py:140-213): storage allocation,
+ *          data stacks seeded with one live slot, pc stack seeded [halt, entry]
+ *   ls_run
+ *       <- pc_vm.run_vm / pc_vm.step (pc_vm.py:304-349): batched block steps
+ *          until every lane halts, StepLimitExceeded, stack faults
+ *   ls_read_output
+ *       <- Machine.output_value (pc_vm.py:136-137): a copy of the output var
+ *   ls_trace_fetch / ls_block_totals
+ *       <- ScheduleTrace.record (metrics.py:36-37), one record per step
+ *   ls_read_var / ls_read_pointers
+ *       <- Machine.stacks / regs / scratch access by observers (pc_vm.py:323)
+ *   ls_rng_uniform
+ *       <- runtime.rng_uniform (runtime.py:288-303)
+ *   ls_target_eval
+ *       <- the logpdf_/grad_ kernels of a TargetDensity (workloads.py:186-228)
+ *
+ * All functions return LS_OK (0) or a negative LS_E* code; ls_last_error()
+ * gives a message. Pointers are plain host pointers unless a name says
+ * "device". One machine is confined to one host thread and one CUDA stream.
+ * There is no CPU execution path: without a CUDA device every compute entry
+ * point fails with LS_ECUDA.
+ */
+#ifndef LOCKSTEP_B200_H
+#define LOCKSTEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LS_ABI_VERSION 1
+
+/* ---- status codes ---------------------------------------------------------- */
+enum {
+  LS_OK = 0,
+  LS_EINVAL = -1,   /* bad argument / malformed program            -> ValueError   */
+  LS_ECUDA = -2,    /* CUDA failure or no device                   -> DeviceError  */
+  LS_ENOMEM = -3,   /* device allocation failed                    -> DeviceError  */
+};
+
+/* ---- run outcome (ls_status.kind) -------------------------------------------- */
+enum {
+  LS_RUN_HALTED = 0,       /* every lane reached the halt block                   */
+  LS_RUN_PAUSED = 1,       /* step budget of this call used, lanes still live     */
+  LS_RUN_OVERFLOW = 2,     /* StackOverflow  (errors.py:54)                        */
+  LS_RUN_UNDERFLOW = 3,    /* StackUnderflow (errors.py:58)                        */
+  LS_RUN_STEP_LIMIT = 4,   /* StepLimitExceeded (errors.py:62)                     */
+};
+
+/* ---- storage classes (compiler.classify_variables) ----------------------------- */
+enum { LS_STACKED = 0, LS_REGISTER = 1, LS_TEMPORARY = 2 };
+
+/* ---- lane kinds (runtime.VType.kind) ---------------------------------------- */
+enum { LS_F64 = 0, LS_I64 = 1, LS_BOOL = 2 };
+
+/* ---- op actions (ir.Push / ir.Update / ir.Pop) ----------------------------- */
+enum { LS_PUSH = 0, LS_UPDATE = 1, LS_POP = 2 };
+
+/* ---- terminators (ir.FlatJump / FlatBranch / PushJump / FlatReturn) --------- */
+enum { LS_JUMP = 0, LS_BRANCH = 1, LS_PUSHJUMP = 2, LS_RETURN = 3 };
+
+/* ---- primitive opcodes (runtime.OPCODES) -------------------------------------- */
+enum ls_opcode {
+  LS_OP_NONE = 0,
+  LS_OP_CONST = 1, LS_OP_ID = 2,
+  LS_OP_ADD = 3, LS_OP_SUB = 4, LS_OP_MUL = 5, LS_OP_DIV = 6, LS_OP_MIN = 7, LS_OP_MAX = 8,
+  LS_OP_LE = 9, LS_OP_LT = 10, LS_OP_EQ = 11,
+  LS_OP_AND = 12, LS_OP_OR = 13, LS_OP_NOT = 14,
+  LS_OP_NEG = 15, LS_OP_ABS = 16,
+  LS_OP_SQRT = 17, LS_OP_EXP = 18, LS_OP_LOG = 19, LS_OP_SIN = 20, LS_OP_COS = 21,
+  LS_OP_FLOOR = 22,
+  LS_OP_SELECT = 23, LS_OP_DOT = 24, LS_OP_AXPY = 25,
+  LS_OP_VGET = 26, LS_OP_VSTORE = 27, LS_OP_VCAT = 28, LS_OP_VFILL = 29, LS_OP_VSLICE = 30,
+  LS_OP_RNG = 31,
+  LS_OP_LOGPDF = 32, LS_OP_GRAD = 33,
+  /* fused superblock: the whole leapfrog function (workloads.py:461-472)
+     executed run-to-return for every selected lane; see DESIGN.md */
+  LS_OP_LEAPFROG = 64,
+};
+
+/* ---- target kinds (workloads.correlated_gaussian / logistic_regression) ------ */
+enum { LS_TARGET_GAUSSIAN = 1, LS_TARGET_LOGREG = 2 };
+
+/* ---- schedule rules ------------------------------------------------------------ */
+enum {
+  LS_SCHED_MIN_PC = 0,          /* reference rule: lowest populated block (pc_vm.py:306-311) */
+  LS_SCHED_MOST_POPULATED = 1,  /* paper's throughput rule: block with most live lanes        */
+};
+
+/* One flat op (ir.Push/Update/Pop). */
+typedef struct {
+  int32_t opcode;   /* enum ls_opcode; LS_OP_NONE for a pop                    */
+  int32_t action;   /* LS_PUSH / LS_UPDATE / LS_POP                             */
+  int32_t out;      /* output var (or popped var)                               */
+  int32_t nin;      /* number of inputs                                         */
+  int32_t in[3];    /* input vars                                               */
+  int32_t kind;     /* lane kind of the first input (polymorphic arithmetic)   */
+  int32_t width;    /* output width in words (1 for scalars)                   */
+  int32_t imm0;     /* vfill width / vslice lo / target slot / leapfrog steps  */
+  int32_t imm1;     /* vslice hi / leapfrog: var of q                          */
+  int32_t imm2;     /* leapfrog: var of p                                       */
+  int64_t bits;     /* const payload (f64 bits or i64)                          */
+} ls_op;
+
+/* One flat block. */
+typedef struct {
+  int32_t op_begin;
+  int32_t op_count;
+  int32_t term;     /* LS_JUMP / LS_BRANCH / LS_PUSHJUMP / LS_RETURN */
+  int32_t a;        /* jump target, branch true target, pushjump jump_to     */
+  int32_t b;        /* branch false target, pushjump return_to               */
+  int32_t cond;     /* branch condition var                                   */
+  int32_t grads;    /* grad-kernel invocations per lane in this block         */
+  int32_t pad;
+} ls_block;
+
+/* One variable. */
+typedef struct {
+  int32_t cls;      /* LS_STACKED / LS_REGISTER / LS_TEMPORARY */
+  int32_t kind;     /* LS_F64 / LS_I64 / LS_BOOL               */
+  int32_t width;    /* words per lane (>= 1)                    */
+  int32_t sp;       /* stack-pointer row for stacked vars, -1 otherwise */
+} ls_var;
+
+typedef struct {
+  const ls_block* blocks; int32_t n_blocks;
+  const ls_op* ops;       int32_t n_ops;
+  const ls_var* vars;     int32_t n_vars;
+  int32_t entry;
+  const int32_t* inputs;  int32_t n_inputs;
+  int32_t output;
+} ls_program_desc;
+
+typedef struct {
+  int32_t sched;          /* LS_SCHED_*                                               */
+  int32_t lanes_per_cta;  /* lanes one VM group (CTA) schedules together; 0 = all Z
+                             lanes in one group (exact reference schedule; Z <= 1024) */
+  int32_t ctas;           /* persistent CTAs; 0 = one wave over all SMs               */
+  int32_t trace;          /* record (block, active) per step (single group only)      */
+  int32_t exact_logpdf;   /* 1: numpy einsum summation order; 0: fused fast form      */
+  int32_t lane_trace_cap; /* >0: record each chain's block sequence (first cap steps) */
+  int32_t reserved[2];
+} ls_machine_opts;
+
+typedef struct {
+  int32_t kind;           /* LS_RUN_*                                          */
+  int32_t var;            /* faulting variable (-1 = the pc stack)             */
+  int64_t lane;           /* faulting lane (lowest index)                      */
+  int32_t block;          /* block executing when the fault hit                */
+  int32_t pad;
+  int64_t steps;          /* steps executed so far (max over groups)           */
+  int64_t useful_grads;   /* sum over steps of active lanes x grad invocations */
+  int64_t launched_grads; /* sum over steps of group lanes x grad invocations  */
+} ls_status;
+
+typedef struct ls_program ls_program;
+typedef struct ls_machine ls_machine;
+
+int ls_abi_version(void);
+const char* ls_last_error(void);
+int ls_device_count(int32_t* n);
+
+int ls_program_create(const ls_program_desc* desc, ls_program** out);
+/* Bind target slot `slot`: gaussian params = P (dim x dim, row-major) and
+   `norm`; logistic params = sx (n x dim, row-major), norm unused. */
+int ls_program_bind_target(ls_program* p, int32_t slot, int32_t kind, int32_t dim,
+                           int32_t n, const double* params, double norm);
+int ls_program_destroy(ls_program* p);
+
+int ls_machine_create(ls_program* p, int64_t z, int32_t depth,
+                      const ls_machine_opts* opts, ls_machine** out);
+/* input `idx` of the program, host array of z * width words (lane-major) */
+int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes);
+/* same, from device memory (e.g. a torch CUDA tensor) */
+int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes);
+/* Execute up to max_steps steps per group (<0: unbounded). Returns LS_OK and
+   fills *st; faults are reported in st->kind, not as an error code. */
+int ls_run(ls_machine* m, int64_t max_steps, ls_status* st);
+int ls_read_output(ls_machine* m, void* host, int64_t bytes);
+/* device pointer of the z x width output (valid until destroy) */
+int ls_output_device(ls_machine* m, void** dev);
+/* drain recorded (block, active) step pairs; *n = number written */
+int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap, int64_t* n);
+/* per-block totals over all groups: steps executed and sum of active lanes */
+int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active);
+/* observer access (single-group machines): all `depth` slots of a var as
+   host array [slots][z][width]; pointers as [z] int64 (stacked vars / -1 = pc) */
+int ls_read_var(ls_machine* m, int32_t var, void* host, int64_t bytes);
+int ls_read_pointers(ls_machine* m, int32_t var, int64_t* host, int64_t z);
+/* the pc stack of a single-group machine as host [depth+1][z] int32 */
+int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count);
+/* per-chain block sequences: blocks [z][cap], lens [z] (a len > cap was truncated) */
+int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap);
+int ls_machine_sync(ls_machine* m);
+int ls_machine_destroy(ls_machine* m);
+
+/* runtime.rng_uniform over n lanes (keys/counters as int64 after numpy's astype) */
+int ls_rng_uniform(const int64_t* key, const int64_t* counter, int64_t n, double* out);
+/* evaluate a target's logpdf (which=0) or grad (which=1) on z points x[z][dim] */
+int ls_target_eval(int32_t kind, int32_t which, int32_t dim, int32_t n, const double* params,
+                   double norm, const double* x, int64_t z, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOCKSTEP_B200_H */

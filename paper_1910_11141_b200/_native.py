@@ -1,0 +1,273 @@
+"""ctypes binding of `include/lockstep_b200.h` (the C ABI of the B200 VM).
+
+This is the only place Python touches the CUDA library. It loads the
+in-tree `_lib/liblockstep_b200.so` and fails loudly (DeviceError) if the
+library or a GPU is missing: there is no CPU fallback behind it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+
+from .errors import DeviceError
+from .lowering import DeviceProgram
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblockstep_b200.so"
+HEADER = Path(__file__).resolve().parent.parent / "include" / "lockstep_b200.h"
+
+LS_OK, LS_EINVAL, LS_ECUDA, LS_ENOMEM = 0, -1, -2, -3
+RUN_HALTED, RUN_PAUSED, RUN_OVERFLOW, RUN_UNDERFLOW, RUN_STEP_LIMIT = 0, 1, 2, 3, 4
+SCHED = {"min_pc": 0, "most_populated": 1}
+
+
+class ProgramDesc(C.Structure):
+    _fields_ = [("blocks", C.c_void_p), ("n_blocks", C.c_int32),
+                ("ops", C.c_void_p), ("n_ops", C.c_int32),
+                ("vars", C.c_void_p), ("n_vars", C.c_int32),
+                ("entry", C.c_int32),
+                ("inputs", C.c_void_p), ("n_inputs", C.c_int32),
+                ("output", C.c_int32)]
+
+
+class MachineOpts(C.Structure):
+    _fields_ = [("sched", C.c_int32), ("lanes_per_cta", C.c_int32), ("ctas", C.c_int32),
+                ("trace", C.c_int32), ("exact_logpdf", C.c_int32), ("lane_trace_cap", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
+
+
+class Status(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("var", C.c_int32), ("lane", C.c_int64),
+                ("block", C.c_int32), ("pad", C.c_int32), ("steps", C.c_int64),
+                ("useful_grads", C.c_int64), ("launched_grads", C.c_int64)]
+
+
+_lib = None
+
+_SIGS = {
+    "ls_abi_version": ([], C.c_int),
+    "ls_last_error": ([], C.c_char_p),
+    "ls_device_count": ([C.POINTER(C.c_int32)], C.c_int),
+    "ls_program_create": ([C.POINTER(ProgramDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "ls_program_bind_target": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_void_p, C.c_double], C.c_int),
+    "ls_program_destroy": ([C.c_void_p], C.c_int),
+    "ls_machine_create": ([C.c_void_p, C.c_int64, C.c_int32, C.POINTER(MachineOpts),
+                           C.POINTER(C.c_void_p)], C.c_int),
+    "ls_machine_set_input": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
+    "ls_machine_set_input_device": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
+    "ls_run": ([C.c_void_p, C.c_int64, C.POINTER(Status)], C.c_int),
+    "ls_read_output": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "ls_output_device": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "ls_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "ls_block_totals": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ls_read_var": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
+    "ls_read_pointers": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
+    "ls_read_pc_stack": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "ls_lane_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "ls_machine_sync": ([C.c_void_p], C.c_int),
+    "ls_machine_destroy": ([C.c_void_p], C.c_int),
+    "ls_rng_uniform": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
+    "ls_target_eval": ([C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_double,
+                        C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
+}
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(ls_\w+)\(", text, re.M)))
+
+
+def load():
+    """Load (never build) the CUDA library; DeviceError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise DeviceError(f"CUDA library {LIB_PATH} is missing; run "
+                          "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> None:
+    if rc != LS_OK:
+        msg = load().ls_last_error().decode(errors="replace")
+        if rc == LS_EINVAL:
+            raise ValueError(msg)
+        raise DeviceError(msg)
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    rc = load().ls_device_count(C.byref(n))
+    return n.value if rc == LS_OK else 0
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+class Program:
+    """Owns an `ls_program` built from a DeviceProgram."""
+
+    def __init__(self, dp: DeviceProgram):
+        lib = load()
+        self.dp = dp
+        self._keep = [np.ascontiguousarray(dp.blocks), np.ascontiguousarray(dp.ops),
+                      np.ascontiguousarray(dp.vars), np.ascontiguousarray(dp.inputs, dtype=np.int32)]
+        b, o, v, i = self._keep
+        desc = ProgramDesc(_ptr(b), len(b), _ptr(o) if len(o) else None, len(o), _ptr(v), len(v),
+                           dp.flat.entry, _ptr(i) if len(i) else None, len(i), dp.output)
+        h = C.c_void_p()
+        _check(lib.ls_program_create(C.byref(desc), C.byref(h)))
+        self.handle = h
+        for slot, t in enumerate(dp.targets):
+            self._bind(slot, t)
+
+    def _bind(self, slot: int, t) -> None:
+        from .workloads import TARGET_GAUSSIAN
+
+        if t.kind == TARGET_GAUSSIAN:
+            params, n, norm = t.params["prec"], t.dim, t.params["norm"]
+        else:
+            params, n, norm = t.params["sx"], t.params["sx"].shape[0], 0.0
+        params = np.ascontiguousarray(params, dtype=np.float64)
+        _check(load().ls_program_bind_target(self.handle, slot, t.kind, t.dim, n, _ptr(params), norm))
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.ls_program_destroy(self.handle)
+            self.handle = None
+
+
+class MachineHandle:
+    """Owns an `ls_machine` (device storage for one batch of lanes)."""
+
+    def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
+                 lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
+                 exact_logpdf: bool = True, lane_trace_cap: int = 0):
+        lib = load()
+        if sched not in SCHED:
+            raise ValueError(f"unknown schedule '{sched}'")
+        self.program = program
+        self.z = z
+        self.depth = depth
+        opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
+                           int(lane_trace_cap))
+        self.lane_trace_cap = int(lane_trace_cap)
+        h = C.c_void_p()
+        _check(lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)))
+        self.handle = h
+
+    def set_input(self, idx: int, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        _check(load().ls_machine_set_input(self.handle, idx, _ptr(arr), arr.nbytes))
+
+    def set_input_device(self, idx: int, dev_ptr: int, nbytes: int) -> None:
+        _check(load().ls_machine_set_input_device(self.handle, idx, C.c_void_p(dev_ptr), nbytes))
+
+    def run(self, max_steps: int) -> Status:
+        st = Status()
+        _check(load().ls_run(self.handle, max_steps, C.byref(st)))
+        return st
+
+    def read_output(self, width: int, dtype) -> np.ndarray:
+        out = np.empty((self.z, width), dtype=np.uint64)
+        _check(load().ls_read_output(self.handle, _ptr(out), out.nbytes))
+        return out.view(dtype)
+
+    def output_device_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(load().ls_output_device(self.handle, C.byref(p)))
+        return p.value
+
+    def fetch_trace(self, cap: int = 1 << 16) -> tuple[np.ndarray, np.ndarray]:
+        blocks, active = [], []
+        while True:
+            b = np.empty(cap, np.int32)
+            a = np.empty(cap, np.int32)
+            n = C.c_int64(0)
+            _check(load().ls_trace_fetch(self.handle, _ptr(b), _ptr(a), cap, C.byref(n)))
+            blocks.append(b[:n.value])
+            active.append(a[:n.value])
+            if n.value < cap:
+                break
+        return np.concatenate(blocks), np.concatenate(active)
+
+    def block_totals(self, n_blocks: int) -> tuple[np.ndarray, np.ndarray]:
+        s = np.zeros(n_blocks, np.int64)
+        a = np.zeros(n_blocks, np.int64)
+        _check(load().ls_block_totals(self.handle, _ptr(s), _ptr(a)))
+        return s, a
+
+    def read_var(self, var: int, slots: int, width: int) -> np.ndarray:
+        out = np.empty((slots, self.z, width), np.uint64)
+        _check(load().ls_read_var(self.handle, var, _ptr(out), out.nbytes))
+        return out
+
+    def read_pointers(self, var: int) -> np.ndarray:
+        out = np.empty(self.z, np.int64)
+        _check(load().ls_read_pointers(self.handle, var, _ptr(out), self.z))
+        return out
+
+    def read_pc_stack(self) -> np.ndarray:
+        out = np.empty((self.depth + 1, self.z), np.int32)
+        _check(load().ls_read_pc_stack(self.handle, _ptr(out), out.size))
+        return out.astype(np.int64)
+
+    def lane_traces(self) -> list[np.ndarray]:
+        cap = self.lane_trace_cap
+        blocks = np.empty((self.z, cap), np.int32)
+        lens = np.empty(self.z, np.int32)
+        _check(load().ls_lane_trace_fetch(self.handle, _ptr(blocks), _ptr(lens), cap))
+        if (lens > cap).any():
+            raise ValueError(f"lane trace truncated: raise lane_trace_cap above {int(lens.max())}")
+        return [blocks[i, :lens[i]].copy() for i in range(self.z)]
+
+    def sync(self) -> None:
+        _check(load().ls_machine_sync(self.handle))
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.ls_machine_destroy(self.handle)
+            self.handle = None
+
+
+def _as_i64(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a).astype(np.int64))
+
+
+def rng_uniform(key: np.ndarray, counter: np.ndarray) -> np.ndarray:
+    """Device evaluation of runtime.rng_uniform (keys/counters cast like numpy astype)."""
+    k, c = np.broadcast_arrays(_as_i64(key), _as_i64(counter))
+    k, c = np.ascontiguousarray(k), np.ascontiguousarray(c)
+    out = np.empty(k.shape, np.float64)
+    _check(load().ls_rng_uniform(_ptr(k), _ptr(c), k.size, _ptr(out)))
+    return out
+
+
+def target_eval(target, which: str, x: np.ndarray) -> np.ndarray:
+    from .workloads import TARGET_GAUSSIAN
+
+    x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+    z = x.shape[0]
+    if target.kind == TARGET_GAUSSIAN:
+        params, n, norm = target.params["prec"], target.dim, target.params["norm"]
+    else:
+        params, n, norm = target.params["sx"], target.params["sx"].shape[0], 0.0
+    params = np.ascontiguousarray(params, dtype=np.float64)
+    w = 0 if which == "logpdf" else 1
+    out = np.empty(z if w == 0 else (z, target.dim), np.float64)
+    _check(load().ls_target_eval(target.kind, w, target.dim, n, _ptr(params), norm, _ptr(x), z,
+                                 _ptr(out)))
+    return out

@@ -1,0 +1,448 @@
+"""Drop-in replacement of the reference engine `lockstep.pc_vm`, on the B200.
+
+Same entry points and semantics as reference `pkg/src/lockstep/pc_vm.py`:
+
+    infer_types(flat, input_types)                           pc_vm.py:49-97
+    init_machine(compiled, inputs, *, depth, mode, trace)    pc_vm.py:140-213
+    step(m, *, observer, debug) -> bool                      pc_vm.py:304-332
+    run_vm(m, *, max_steps, observer, debug)                 pc_vm.py:338-349
+    run_flat(...), run(...) -> (outputs, ScheduleTrace)      pc_vm.py:352-383
+    check_coherence(m)                                       pc_vm.py:391-400
+
+Every block step executes in the CUDA VM (`csrc/vm.cu`) through the C ABI;
+this module only moves inputs/outputs, maps status codes to the reference
+exceptions and rebuilds `ScheduleTrace` records from the device trace.
+
+Schedules. With Z <= 1024 lanes and no `lanes_per_group`, all lanes form one
+schedule group and the device applies the reference's min-pc rule, so the
+global step sequence (and every frozen step count) equals the reference's.
+Larger batches are split into groups of `lanes_per_group` lanes (one CTA
+each) that schedule independently and refill lanes from a chain queue; each
+lane's results are unchanged (lane isolation, reference runtime.py:96-104),
+and the returned trace carries per-block totals instead of a step list.
+
+`mode` ("masked" / "gather") is accepted for API compatibility: the device
+always computes only the selected lanes, which the reference guarantees to
+be bit-identical to masked execution (test_acceptance.py:177-198).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, ir
+from .compiler import CompiledProgram
+from .errors import (StackFault, StackOverflow, StackUnderflow, StepLimitExceeded,
+                     TypeInferenceError)
+from .lowering import DeviceProgram, lower
+from .metrics import ScheduleTrace
+from .runtime import BOOL, I64, VType, batch, resolve_kernel, vtype_of
+
+DEFAULT_MAX_STEPS = 1_000_000
+MAX_GROUP_LANES = 1024
+
+
+# ---- type inference (reference pc_vm.py:49-97) ----------------------------------------
+
+
+def infer_types(flat: ir.FlatProgram, input_types: list[VType]) -> dict[str, VType]:
+    """Forward fixpoint of one static type per variable, seeded by the inputs."""
+    if len(input_types) != len(flat.inputs):
+        raise TypeInferenceError(f"program wants {len(flat.inputs)} inputs, got {len(input_types)}")
+    types: dict[str, VType] = dict(zip(flat.inputs, input_types))
+    changed = True
+    while changed:
+        changed = False
+        for blk in flat.blocks:
+            for op in blk.ops:
+                if isinstance(op, ir.Pop):
+                    continue
+                ins = [types.get(v) for v in op.inputs]
+                if any(t is None for t in ins):
+                    continue
+                try:
+                    vt = resolve_kernel(op.prim.name).type_rule(tuple(ins))
+                except ValueError as e:
+                    raise TypeInferenceError(
+                        f"'{op.prim.name}' on {tuple(map(str, ins))}: {e}") from None
+                old = types.get(op.output)
+                if old is None:
+                    types[op.output] = vt
+                    changed = True
+                elif old != vt:
+                    raise TypeInferenceError(f"variable '{op.output}' is both {old} and {vt}")
+    for blk in flat.blocks:
+        t = blk.terminator
+        if isinstance(t, ir.FlatBranch):
+            ct = types.get(t.cond)
+            if ct is not None and ct != BOOL:
+                raise TypeInferenceError(f"branch condition '{t.cond}' has type {ct}, wants bool")
+    return types
+
+
+# ---- host views of device storage (for observers) -------------------------------------------
+
+
+def _decode(raw: np.ndarray, vt: VType) -> np.ndarray:
+    if vt.kind == "f64":
+        arr = raw.view(np.float64)
+    elif vt.kind == "i64":
+        arr = raw.view(np.int64)
+    else:
+        arr = raw != 0
+    return arr if vt.width else arr[..., 0]
+
+
+class StackView:
+    """Read-only snapshot of one stacked variable, shaped like runtime.StackedVar."""
+
+    def __init__(self, name: str, depth: int, z: int, vt: VType, data: np.ndarray, pointers: np.ndarray):
+        self.name, self.depth, self.z, self.vt = name, depth, z, vt
+        self.data = data
+        self.pointers = pointers
+
+    @property
+    def cached_top(self) -> np.ndarray:
+        slot = np.maximum(self.pointers - 1, 0)
+        return self.data[slot, np.arange(self.z)]
+
+
+class _Views:
+    def __init__(self, m: "Machine", cls: str):
+        self.m, self.cls = m, cls
+
+    def _names(self):
+        return [v for v, c in self.m.classes.items() if c == self.cls]
+
+    def __contains__(self, name):
+        return self.m.classes.get(name) == self.cls
+
+    def __iter__(self):
+        return iter(self._names())
+
+    def keys(self):
+        return self._names()
+
+    def values(self):
+        return [self[n] for n in self._names()]
+
+    def items(self):
+        return [(n, self[n]) for n in self._names()]
+
+    def __len__(self):
+        return len(self._names())
+
+    def __getitem__(self, name: str):
+        if self.m.classes.get(name) != self.cls:
+            raise KeyError(name)
+        return self.m._view(name)
+
+
+class GroupTrace(ScheduleTrace):
+    """Trace of a multi-group run: per-block totals instead of one record per step.
+
+    `block_steps[b]` counts group-steps of block b summed over groups,
+    `block_active[b]` the active lanes they carried; `lanes` is the group width.
+    """
+
+    def __init__(self, engine: str, z: int, labels, prims, lanes: int,
+                 block_steps: np.ndarray, block_active: np.ndarray):
+        super().__init__(engine=engine, z=z)
+        self.labels, self.block_prims, self.lanes = labels, prims, lanes
+        self.block_steps, self.block_active = block_steps, block_active
+
+    @property
+    def step_count(self) -> int:
+        return int(self.block_steps.sum())
+
+    def _per_block(self, counted):
+        return np.array([sum(n for k, n in p.items() if counted is None or k in counted)
+                         for p in self.block_prims], dtype=np.int64)
+
+    def invocations(self, counted=None) -> int:
+        return int((self.block_steps * self._per_block(counted)).sum())
+
+    def useful_invocations(self, counted=None) -> int:
+        return int((self.block_active * self._per_block(counted)).sum())
+
+    def occupancy(self, counted=None) -> tuple[int, int]:
+        c = self._per_block(counted)
+        return int((self.block_active * c).sum()), int((self.block_steps * c).sum()) * self.lanes
+
+
+# ---- the machine ----------------------------------------------------------------------------
+
+
+class Machine:
+    """A batch of Z lanes resident on the GPU (reference `Machine`, pc_vm.py:103-137)."""
+
+    def __init__(self, compiled: CompiledProgram, dp: DeviceProgram, handle: _native.MachineHandle,
+                 z: int, depth: int, mode: str, types, trace: ScheduleTrace | None,
+                 schedule: str, groups_exact: bool, lanes: int):
+        self.flat = compiled.flat
+        self.classes = dp.classes
+        self.labels = compiled.labels
+        self.z, self.depth, self.mode, self.types = z, depth, mode, types
+        self.trace = trace
+        self.steps = 0
+        self.schedule = schedule
+        self.exact = groups_exact
+        self.lanes = lanes
+        self._dp = dp
+        self._h = handle
+        self._useful = 0
+        self._launched = 0
+        self.stacks = _Views(self, "stacked")
+        self.regs = _Views(self, "register")
+        self.scratch = _Views(self, "temporary")
+        self.halted = False
+
+    @property
+    def halt_index(self) -> int:
+        return self.flat.halt_index
+
+    def lane_traces(self) -> list[np.ndarray]:
+        """Each lane's executed block sequence (needs lane_trace_cap > 0 at init)."""
+        return self._h.lane_traces()
+
+    @property
+    def useful_grads(self) -> int:
+        """Sum over steps of active lanes x grad invocations (the headline unit)."""
+        return self._useful
+
+    def _need_exact(self):
+        if not self.exact:
+            raise ValueError("machine state views need a single schedule group (Z <= 1024)")
+
+    def _view(self, name: str):
+        self._need_exact()
+        vid = self._dp.var_index[name]
+        vt = self._dp.types[name]
+        cls = self.classes[name]
+        slots = self.depth if cls == "stacked" else 1
+        raw = self._h.read_var(vid, slots, vt.words)
+        data = _decode(raw, vt)
+        if cls == "stacked":
+            return StackView(name, self.depth, self.z, vt, data, self._h.read_pointers(vid))
+        return data[0]
+
+    @property
+    def pc(self) -> StackView:
+        self._need_exact()
+        data = self._h.read_pc_stack()
+        return StackView("$pc", self.depth + 1, self.z, I64, data, self._h.read_pointers(-1))
+
+    def value_of(self, var: str) -> np.ndarray:
+        v = self._view(var)
+        return v.cached_top if isinstance(v, StackView) else v
+
+    def pc_tops(self) -> np.ndarray:
+        return self.pc.cached_top
+
+    def active_mask(self) -> np.ndarray:
+        if self.exact:
+            return self.pc_tops() != self.halt_index
+        return np.zeros(self.z, bool) if self.halted else np.ones(self.z, bool)
+
+    def output_value(self) -> np.ndarray:
+        if self.halted or not self.exact:
+            vt = self._dp.types[self.flat.output]
+            return _decode(self._h.read_output(vt.words, np.uint64).reshape(self.z, vt.words), vt).copy()
+        return np.array(self.value_of(self.flat.output), copy=True)
+
+
+def _prepare_inputs(flat: ir.FlatProgram, inputs) -> list[np.ndarray]:
+    arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
+    if len(arrays) != len(flat.inputs):
+        raise ValueError(f"program wants {len(flat.inputs)} inputs, got {len(arrays)}")
+    if not arrays:
+        raise ValueError("program must take at least one input")
+    z = arrays[0].shape[0]
+    if any(a.shape[0] != z for a in arrays):
+        raise ValueError("all inputs must share the batch width")
+    if z < 1:
+        raise ValueError("batch width must be at least 1")
+    return arrays
+
+
+def _as_words(a: np.ndarray) -> np.ndarray:
+    if a.dtype == np.bool_:
+        a = a.astype(np.uint64)
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64).reshape(a.shape[0], -1)
+
+
+def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
+                 trace: ScheduleTrace | None = None, schedule: str = "min_pc",
+                 lanes_per_group: int | None = None, groups: int = 0,
+                 optimize: bool = False, exact_logpdf: bool = True,
+                 lane_trace_cap: int = 0) -> Machine:
+    """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
+
+    Data stacks get `depth` slots with one live slot per lane; inputs land in
+    that slot; the pc stack gets depth+1 slots seeded [halt, entry].
+    """
+    if mode not in ("masked", "gather"):
+        raise ValueError(f"unknown mode '{mode}'")
+    if depth < 1:
+        raise ValueError("stack depth must be at least 1")
+    flat = compiled.flat
+    arrays = _prepare_inputs(flat, inputs)
+    z = arrays[0].shape[0]
+    types = infer_types(flat, [vtype_of(a) for a in arrays])
+    dp = lower(compiled, types, optimize=optimize)
+    program = _native.Program(dp)
+    exact = lanes_per_group is None and z <= MAX_GROUP_LANES
+    if lanes_per_group is None and not exact:
+        lanes_per_group = 256
+    handle = _native.MachineHandle(program, z, depth, sched=schedule,
+                                   lanes_per_cta=0 if exact else int(lanes_per_group),
+                                   ctas=groups, trace=exact and trace is not None,
+                                   exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap)
+    for k, a in enumerate(arrays):
+        handle.set_input(k, _as_words(a))
+    lanes = z if exact else int(lanes_per_group)
+    return Machine(compiled, dp, handle, z, depth, mode, types, trace, schedule, exact, lanes)
+
+
+def _raise_fault(m: Machine, st) -> None:
+    label = m.labels[st.block] if 0 <= st.block < len(m.labels) else None
+    if st.var < 0:
+        name, cap = "$pc", m.depth + 1
+    else:
+        name, cap = m._dp.var_names[st.var], m.depth
+    if st.kind == _native.RUN_OVERFLOW:
+        err: StackFault = StackOverflow(name, int(st.lane), f"depth {cap}")
+    else:
+        err = StackUnderflow(name, int(st.lane), "update on empty stack" if st.pad == 1 else "")
+    err.block = label
+    raise err
+
+
+def _record(m: Machine, blocks: np.ndarray, active: np.ndarray) -> None:
+    tr = m.trace
+    if tr is None or isinstance(tr, GroupTrace):
+        return
+    labels, prims, sops = m.labels, m._dp.block_prims, m._dp.block_stack_ops
+    for b, n in zip(blocks.tolist(), active.tolist()):
+        tr.record(labels[b], n, prims[b])
+        for var, kind in sops[b]:
+            tr.record_stack_op(var, kind)
+
+
+def _absorb(m: Machine, st) -> None:
+    m.steps = int(st.steps)
+    m._useful = int(st.useful_grads)
+    m._launched = int(st.launched_grads)
+    if m.exact and m.trace is not None:
+        b, a = m._h.fetch_trace()
+        _record(m, b, a)
+
+
+def step(m: Machine, *, observer=None, debug: bool = False) -> bool:
+    """Execute one batched block on the device; False once every lane has halted."""
+    m._need_exact()
+    tops = m.pc_tops()
+    active = tops != m.halt_index
+    if not active.any():
+        m.halted = True
+        return False
+    if m.schedule == "min_pc":
+        b = int(tops[active].min())
+    else:
+        vals, counts = np.unique(tops[active], return_counts=True)
+        b = int(vals[np.argmax(counts)])
+    sel = active & (tops == b)
+    st = m._h.run(m.steps + 1)
+    if st.kind in (_native.RUN_OVERFLOW, _native.RUN_UNDERFLOW):
+        _absorb(m, st)
+        _raise_fault(m, st)
+    _absorb(m, st)
+    if observer is not None:
+        observer(m, b, sel)
+    if debug:
+        check_coherence(m)
+        new = m.pc_tops()
+        if (new[~active] != m.halt_index).any():
+            raise AssertionError("halted lane resumed execution")
+        if ((new < 0) | (new > m.halt_index)).any():
+            raise AssertionError("pc top left the block range")
+    return True
+
+
+def run_vm(m: Machine, *, max_steps: int | None = DEFAULT_MAX_STEPS, observer=None,
+           debug: bool = False) -> np.ndarray:
+    """Step until every lane halts; returns the output batch (reference pc_vm.py:338-349)."""
+    if observer is not None or debug:
+        while step(m, observer=observer, debug=debug):
+            if max_steps is not None and m.steps >= max_steps and m.active_mask().any():
+                raise StepLimitExceeded(max_steps)
+        return m.output_value()
+    limit = -1 if max_steps is None else int(max_steps)
+    while True:
+        st = m._h.run(limit)
+        _absorb(m, st)
+        if st.kind == _native.RUN_HALTED:
+            break
+        if st.kind in (_native.RUN_OVERFLOW, _native.RUN_UNDERFLOW):
+            _raise_fault(m, st)
+        if st.kind == _native.RUN_STEP_LIMIT:
+            raise StepLimitExceeded(max_steps)
+        # RUN_PAUSED: trace buffer drained by _absorb; continue
+    m.halted = True
+    if isinstance(m.trace, GroupTrace):
+        m.trace.block_steps, m.trace.block_active = m._h.block_totals(len(m.flat.blocks))
+    return m.output_value()
+
+
+def run_flat(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
+             max_steps: int | None = DEFAULT_MAX_STEPS, trace: ScheduleTrace | None = None,
+             observer=None, debug: bool = False, **engine) -> np.ndarray:
+    """init_machine + run_vm."""
+    engine.setdefault("optimize", observer is None and not debug)
+    m = init_machine(compiled, inputs, depth=depth, mode=mode, trace=trace, **engine)
+    return run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
+
+
+def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
+        max_steps: int | None = DEFAULT_MAX_STEPS, observer=None, debug: bool = False,
+        schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
+        optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
+        return_machine: bool = False):
+    """Execute a compiled program on the B200; returns (outputs, trace)."""
+    arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
+    z = arrays[0].shape[0] if arrays else 0
+    exact = lanes_per_group is None and z <= MAX_GROUP_LANES
+    if optimize is None:
+        optimize = observer is None and not debug
+    tr: ScheduleTrace = ScheduleTrace(engine="pc", z=z)
+    m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
+                     lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
+                     exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap)
+    if not exact:
+        m.trace = GroupTrace("pc", z, compiled.labels, m._dp.block_prims, m.lanes,
+                             np.zeros(len(compiled.flat.blocks), np.int64),
+                             np.zeros(len(compiled.flat.blocks), np.int64))
+    out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
+    if return_machine:
+        return out, m.trace, m
+    return out, m.trace
+
+
+def trace_flat(compiled: CompiledProgram, inputs, *, depth: int, **kwargs):
+    return run(compiled, inputs, depth=depth, **kwargs)
+
+
+def check_coherence(m: Machine) -> None:
+    """Debug invariant of the reference (pc_vm.py:391-400).
+
+    The device keeps no separate cached top (the top is read from the slot
+    under the pointer), so coherence reduces to pointers staying in range.
+    """
+    for name in list(m.stacks):
+        sv = m.stacks[name]
+        if ((sv.pointers < 0) | (sv.pointers > sv.depth)).any():
+            raise AssertionError(f"stack pointer out of range on '{name}'")
+    pc = m.pc
+    if ((pc.pointers < 0) | (pc.pointers > pc.depth)).any():
+        raise AssertionError("pc stack pointer out of range")
