@@ -1,0 +1,308 @@
+"""Parity of the B200 VM with the reference, through the C ABI (needs a GPU).
+
+Mirrors the reference suites test_pc_vm.py and test_acceptance.py. Integer
+and control results (outputs of integer programs, global step traces,
+per-lane program-counter traces, stack-op counts, fault reports, rng) must
+be bit-exact; float chain positions agree within the tolerance stated per
+test (the reference gradient goes through OpenBLAS, which is not
+reproducible even across its own batch widths — SURVEY.md §0.4).
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_1910_11141_b200 as L
+from paper_1910_11141_b200 import _native, pc_vm
+from paper_1910_11141_b200.compiler import CompileOptions
+from paper_1910_11141_b200.errors import StackOverflow, StepLimitExceeded
+from conftest import load_npz, nuts_program, oracle_run, split_lanes
+
+pytestmark = pytest.mark.gpu
+
+Z_CYCLE = (1, 2, 4, 7, 32)
+ALL_OPTIONS = [CompileOptions(*bits) for bits in itertools.product([True, False], repeat=4)]
+SPIN = "def spin(n) { while (0 <= n) { n = n + 1; } return n; }"
+# float tolerance for whole chains (many leapfrog steps); per-step is 1e-12 below
+CHAIN_RTOL = 1e-9
+
+
+def assert_matches(got, ref, label, rtol=1e-12):
+    if got.dtype.kind in "ib":
+        assert np.array_equal(got, ref), label
+    else:
+        np.testing.assert_allclose(got, ref, rtol=rtol, atol=0.0, err_msg=label)
+
+
+def test_device_present():
+    assert _native.device_count() >= 1
+
+
+def test_corpus_golden_runs(golden_meta, corpus_compiled):
+    g = load_npz("corpus_runs.npz")
+    for name, meta in golden_meta["corpus"].items():
+        _, _, cp = corpus_compiled[name]
+        for run in meta["runs"]:
+            ins = [g[f"{run['tag']}_in{k}"] for k in range(run["n_inputs"])]
+            out, tr = L.run(cp, ins, depth=64)
+            want = g[f"{run['tag']}_out"]
+            assert_matches(out, want, run["tag"])
+            assert [[s.block, s.active] for s in tr.steps] == run["steps"], run["tag"]
+            assert tr.stack_ops == run["stack_ops"], run["tag"]
+
+
+def test_fifty_random_batches_per_program(corpus_compiled):
+    """TestOracleEquivalence (reference test_acceptance.py:54-74) against the oracle."""
+    rng = np.random.default_rng(2024)
+    for name, (e, cfg, _) in corpus_compiled.items():
+        variants = {}
+        for b in range(50 if name != "nuts_lite" else 15):
+            z = Z_CYCLE[b % len(Z_CYCLE)]
+            ins = e.make_inputs(rng, z)
+            opts = ALL_OPTIONS[b % len(ALL_OPTIONS)]
+            if opts not in variants:
+                variants[opts] = L.compile_program(cfg, opts)
+            ref = oracle_run(variants[opts], ins, 64).output
+            got, _ = L.run(variants[opts], ins, depth=64)
+            assert_matches(got, ref, f"{name} batch {b}")
+
+
+def test_all_sixteen_pass_subsets_bit_identical(corpus_compiled):
+    rng = np.random.default_rng(5)
+    for name, (e, cfg, _) in corpus_compiled.items():
+        ins = e.make_inputs(rng, 4)
+        outs = {L.run(L.compile_program(cfg, o), ins, depth=64)[0].tobytes() for o in ALL_OPTIONS}
+        assert len(outs) == 1, name
+
+
+@pytest.mark.parametrize("ins,want", [([3, 7, 4, 5], [3, 21, 5, 8]), ([6, 7, 8, 9], [13, 21, 34, 55])])
+def test_fib_goldens(corpus_compiled, ins, want):
+    out, tr = L.run(corpus_compiled["fibonacci"][2], [np.array(ins)], depth=32)
+    assert out.tolist() == want
+    assert tr.engine == "pc" and tr.z == 4
+
+
+@pytest.mark.parametrize("k,want", [(4, 45), (6, 123), (8, 327)])
+def test_cross_depth_frozen_step_counts(corpus_compiled, k, want):
+    """Frozen pc step counts of reference test_acceptance.py:106-129, plus depth mixing."""
+    mixed = []
+
+    def observer(m, b, sel):
+        ptr = m.stacks["fibonacci.n"].pointers
+        mixed.append(len(np.unique(ptr[sel])) > 1)
+
+    _, tr = L.run(corpus_compiled["fibonacci"][2], [np.array([k, k + 1])], depth=48, observer=observer)
+    assert tr.step_count == want
+    assert any(mixed)
+    _, fast = L.run(corpus_compiled["fibonacci"][2], [np.array([k, k + 1])], depth=48)
+    assert fast.step_count == want
+
+
+def test_loop_programs_touch_no_data_stack(corpus_compiled):
+    for name, args in (("countdown", [7]), ("poly", [3]), ("twosite", [9])):
+        _, tr = L.run(corpus_compiled[name][2], [np.array(args)], depth=16)
+        assert tr.stack_ops == {}
+
+
+def test_stack_traffic_and_balance(corpus_compiled):
+    _, tr = L.run(corpus_compiled["fibonacci"][2], [np.array([8, 3, 6])], depth=32)
+    assert set(tr.stack_ops) == {"fibonacci.n", "fibonacci.left", "fibonacci._ret"}
+    for var, ops in tr.stack_ops.items():
+        assert ops["push"] == ops["pop"], var
+
+
+def test_overflow_names_lane_variable_and_block(corpus_compiled):
+    fib = corpus_compiled["fibonacci"][2]
+    with pytest.raises(StackOverflow) as ei:
+        L.run(fib, [np.array([10])], depth=3)
+    err = ei.value
+    assert err.lane == 0 and err.variable.startswith("fibonacci.")
+    assert err.block is not None and err.block.startswith("fibonacci.")
+    assert "stack overflow" in str(err) and "lane 0" in str(err)
+    with pytest.raises(StackOverflow) as ei:
+        L.run(fib, [np.array([1, 10, 1])], depth=3)
+    assert ei.value.lane == 1
+    with pytest.raises(StackOverflow):
+        L.run(fib, [np.array([10])], depth=2)
+
+
+def test_fault_report_matches_oracle(corpus_compiled):
+    from oracle.lockstep_oracle import OracleFault
+
+    fib = corpus_compiled["fibonacci"][2]
+    for ins in ([np.array([10])], [np.array([1, 10, 1])], [np.array([9, 10, 3, 12])]):
+        with pytest.raises(OracleFault) as want:
+            oracle_run(fib, ins, 3)
+        with pytest.raises(StackOverflow) as got:
+            L.run(fib, ins, depth=3)
+        assert (got.value.variable, got.value.lane, got.value.block) == \
+            (want.value.variable, want.value.lane, want.value.block)
+
+
+def test_step_limit():
+    cp = L.compile_program(L.compile_source(SPIN))
+    with pytest.raises(StepLimitExceeded) as ei:
+        L.run(cp, [np.array([0, 5])], depth=8, max_steps=250)
+    assert ei.value.limit == 250
+    with pytest.raises(StepLimitExceeded):
+        L.run(cp, [np.array([0])], depth=8, max_steps=1000)
+
+
+def test_gather_and_masked_modes_agree(corpus_compiled):
+    ins = [np.array([9, 2, 7, 4])]
+    a, ta = L.run(corpus_compiled["fibonacci"][2], ins, depth=32, mode="masked")
+    b, tb = L.run(corpus_compiled["fibonacci"][2], ins, depth=32, mode="gather")
+    assert a.tobytes() == b.tobytes() and ta.steps == tb.steps and ta.stack_ops == tb.stack_ops
+    with pytest.raises(ValueError):
+        L.run(corpus_compiled["fibonacci"][2], [np.array([1])], depth=8, mode="simd")
+
+
+def test_debug_mode_and_observer(corpus_compiled):
+    for name, (e, _, cp) in corpus_compiled.items():
+        if name == "nuts_lite":
+            continue
+        ins = e.make_inputs(np.random.default_rng(3), 3)
+        L.run(cp, ins, depth=64, debug=True)
+    seen = []
+    _, tr = L.run(corpus_compiled["fibonacci"][2], [np.array([5])], depth=16,
+                  observer=lambda m, b, sel: seen.append(b))
+    assert len(seen) == tr.step_count
+
+
+def test_machine_seeding_and_prebuilt_run(corpus_compiled):
+    fib = corpus_compiled["fibonacci"][2]
+    m = pc_vm.init_machine(fib, [np.array([4, 4])], depth=8)
+    assert m.pc.pointers.tolist() == [2, 2]
+    assert m.pc.data[0].tolist() == [m.halt_index] * 2
+    assert m.pc.data[1].tolist() == [0, 0]
+    m = pc_vm.init_machine(fib, [np.array([6])], depth=16)
+    assert pc_vm.run_vm(m).tolist() == [13]
+    assert not m.active_mask().any()
+    out, _ = L.run(fib, [np.array([0, 9])], depth=32)
+    assert out.tolist() == [1, 55]
+
+
+def test_rng_known_answers_on_device():
+    g = load_npz("rng_kat.npz")
+    assert L.runtime.rng_uniform(g["keys"], g["ctrs"]).tobytes() == g["u"].tobytes()
+    assert L.runtime.rng_uniform(g["fkeys"], g["fctrs"]).tobytes() == g["fu"].tobytes()
+    u = L.runtime.rng_uniform(np.arange(20000), np.zeros(20000, np.int64))
+    assert ((u >= 0) & (u < 1)).all() and abs(u.mean() - 0.5) < 0.01
+
+
+def test_gaussian_target_kernels_on_device():
+    """logpdf in numpy's einsum order is bit-exact; grad within 1e-12 (OpenBLAS order)."""
+    e = load_npz("gauss_logpdf.npz")
+    for d in (2, 5, 25, 100, 128):
+        t = L.correlated_gaussian(d, 0.5)
+        x = e[f"x{d}"]
+        lp = L.runtime.resolve_kernel(t.logpdf).fn((x,), 4)
+        assert lp.tobytes() == e[f"lp{d}"].tobytes(), d
+        g = L.runtime.resolve_kernel(t.grad).fn((x,), 4)
+        np.testing.assert_allclose(g, e[f"g{d}"], rtol=1e-12, atol=1e-14)
+
+
+def test_logreg_target_kernels_on_device():
+    g = load_npz("logreg.npz")
+    for n, d, seed in ((25, 3, 2), (200, 5, 7), (1000, 25, 0)):
+        t = L.logistic_regression(n, d, seed)
+        tag = f"lr{n}x{d}s{seed}"
+        w = g[f"{tag}_w"]
+        np.testing.assert_allclose(L.runtime.resolve_kernel(t.logpdf).fn((w,), 6), g[f"{tag}_lp"], rtol=1e-12)
+        np.testing.assert_allclose(L.runtime.resolve_kernel(t.grad).fn((w,), 6), g[f"{tag}_g"],
+                                   rtol=1e-10, atol=1e-12)
+
+
+def test_gradients_match_finite_differences():
+    """reference test_acceptance.py:273-292, on the device kernels."""
+    for t in (L.correlated_gaussian(2, 0.5), L.correlated_gaussian(3, -0.2),
+              L.logistic_regression(200, 5, seed=7)):
+        lp = L.runtime.resolve_kernel(t.logpdf).fn
+        gr = L.runtime.resolve_kernel(t.grad).fn
+        pts = np.random.default_rng(1).normal(size=(10, t.dim))
+        g = gr((pts,), 10)
+        h = 1e-6
+        for i in range(t.dim):
+            e = np.zeros(t.dim)
+            e[i] = h
+            fd = (lp((pts + e,), 10) - lp((pts - e,), 10)) / (2 * h)
+            rel = np.abs(g[:, i] - fd) / np.maximum(np.abs(fd), 1e-12)
+            assert rel.max() < 1e-5, (t.name, i, rel.max())
+
+
+def test_leapfrog_per_step_tolerance():
+    """Single leaves (L steps) against reference vectors: 1e-12 relative per step."""
+    g = load_npz("leapfrog.npz")
+    for d, steps in ((2, 1), (2, 4), (100, 1), (100, 4)):
+        _, _, cp = nuts_program({"dim": d, "rho": 0.5, "config": dict(leaf_steps=steps, max_depth=6,
+                                                                    iterations=1)}, entry="leapfrog")
+        tag = f"d{d}_L{steps}"
+        got, _ = L.run(cp, [g[f"{tag}_q"], g[f"{tag}_p"], g[f"{tag}_e"]], depth=4)
+        want = g[f"{tag}_out"]
+        err = np.abs(got - want) / np.maximum(np.abs(want), 1e-300)
+        assert (err <= 1e-12 * steps).all() or np.abs(got - want).max() < 1e-13, (tag, err.max())
+
+
+def test_leapfrog_is_reversible():
+    _, _, cp = nuts_program({"dim": 2, "rho": 0.5, "config": dict(max_depth=6, iterations=1)},
+                            entry="leapfrog")
+    rng = np.random.default_rng(101)
+    q0, p0, eps = rng.normal(size=(1, 2)), rng.normal(size=(1, 2)), np.array([0.25])
+    fwd, _ = L.run(cp, [q0, p0, eps], depth=4)
+    back, _ = L.run(cp, [fwd[:, :2], -fwd[:, 2:], eps], depth=4)
+    assert np.abs(back[:, :2] - q0).max() < 1e-10 and np.abs(back[:, 2:] + p0).max() < 1e-10
+
+
+@pytest.mark.parametrize("case", ["nuts_d2", "nuts_d5", "nuts_d3m", "nuts_d100"])
+def test_nuts_golden_traces_exact_and_chains_close(golden_meta, case):
+    meta = golden_meta["nuts"][case]
+    g = load_npz("nuts_runs.npz")
+    cfg, t, cp = nuts_program(meta)
+    z, d = meta["z"], meta["dim"]
+    ins = [np.zeros((z, d)), g[f"{case}_key"]]
+    out, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, lane_trace_cap=1 << 16,
+                       return_machine=True)
+    # control: global schedule, per-lane pc sequences and stack traffic are exact
+    assert np.array_equal(np.array([[cp.labels.index(s.block), s.active] for s in tr.steps], np.int32),
+                          g[f"{case}_steps"])
+    want_lanes = split_lanes(g[f"{case}_lane_len"], g[f"{case}_lane_blocks"])
+    for lane, seq in enumerate(m.lane_traces()):
+        assert np.array_equal(seq, want_lanes[lane]), lane
+    assert tr.stack_ops == meta["stack_ops"]
+    assert m.useful_grads == meta["useful_grads"] == tr.useful_invocations({t.grad})
+    # positions: accumulated over every leapfrog step of the run
+    want = g[f"{case}_out"]
+    scale = np.maximum(np.abs(want), 1.0)
+    assert (np.abs(out - want) / scale).max() < CHAIN_RTOL
+
+
+@pytest.mark.parametrize("lanes,sched", [(32, "min_pc"), (64, "most_populated"), (128, "min_pc"),
+                                         (256, "most_populated")])
+def test_multi_group_schedules_do_not_change_lanes(lanes, sched):
+    """Lane isolation: any grouping/schedule gives each chain bit-identical results."""
+    cfg, t, cp = nuts_program({"dim": 5, "rho": 0.5, "config": dict(max_depth=8, iterations=4)})
+    z = 1500
+    ins = [np.zeros((z, 5)), np.arange(z, dtype=np.int64) * 104729 + 3]
+    base, _ = L.run(cp, [ins[0][:64], ins[1][:64]], depth=cfg.min_stack_depth)
+    got, tr = L.run(cp, ins, depth=cfg.min_stack_depth, lanes_per_group=lanes, schedule=sched)
+    assert got[:64].tobytes() == base.tobytes()
+    ref = oracle_run(cp, [ins[0][64:96], ins[1][64:96]], cfg.min_stack_depth).output
+    assert (np.abs(got[64:96] - ref) / np.maximum(np.abs(ref), 1.0)).max() < CHAIN_RTOL
+    assert tr.useful_invocations({t.grad}) > 0
+    assert 0 < L.utilization(tr, {t.grad}) <= 1
+
+
+def test_sampler_statistics():
+    """reference test_acceptance.py:205-233: 64 lanes x 400 iterations recover the moments."""
+    cfg = L.NutsConfig(step_size=0.25, leaf_steps=4, max_depth=6, iterations=400, seed=0)
+    t = L.correlated_gaussian(2, 0.5)
+    cp = L.compile_program(L.compile_source(L.nuts_lite_source(cfg, t), "nuts_main"))
+    z = 64
+    key = np.random.default_rng(cfg.seed).integers(0, 2**31, size=z).astype(np.int64)
+    flat, _ = L.run(cp, [np.zeros((z, 2)), key], depth=cfg.min_stack_depth)
+    samples = L.workloads.chain_array(flat, cfg, 2).reshape(-1, 2)
+    mean = samples.mean(axis=0)
+    cov = np.cov(samples.T)
+    assert np.abs(mean).max() < 0.1
+    assert np.abs(cov - t.cov).max() < 0.15
