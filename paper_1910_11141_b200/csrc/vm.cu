@@ -791,6 +791,8 @@ int ls_machine_destroy(ls_machine* m) {
   return LS_OK;
 }
 
+static int static_init(ls_machine* m);
+
 int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_opts* opts,
                       ls_machine** out) {
   if (!p || !out || z < 1 || depth < 1) return fail(LS_EINVAL, "bad machine arguments");
@@ -908,6 +910,10 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   }
   CK(cudaStreamSynchronize(m->stream));
   CK(cudaGetLastError());
+  if ((rc = static_init(m))) {
+    ls_machine_destroy(m);
+    return rc;
+  }
   *out = m;
   return LS_OK;
 }
@@ -918,7 +924,7 @@ int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t b
   if (bytes != want) return fail(LS_EINVAL, "input size mismatch");
   CK(cudaMemcpyAsync(m->inputs[idx], host, bytes, cudaMemcpyHostToDevice, m->stream));
   CK(cudaStreamSynchronize(m->stream));
-  return LS_OK;
+  return static_init(m);
 }
 
 int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes) {
@@ -926,7 +932,7 @@ int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int
   const int64_t want = m->z * m->input_width[idx] * 8;
   if (bytes != want) return fail(LS_EINVAL, "input size mismatch");
   CK(cudaMemcpyAsync(m->inputs[idx], dev, bytes, cudaMemcpyDeviceToDevice, m->stream));
-  return LS_OK;
+  return static_init(m);
 }
 
 __global__ void init_static_kernel(const __grid_constant__ VMArgs a) {
@@ -966,14 +972,23 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   return a;
 }
 
+// Single-group machines are seeded eagerly (pc stack [halt, entry], one live
+// slot per data stack, inputs in slot 0) so observers can inspect them before
+// the first step; refilling machines seed each lane when it takes a chain.
+static int static_init(ls_machine* m) {
+  VMArgs a = make_args(m, 0);
+  if (a.refill || m->started) return LS_OK;
+  init_static_kernel<<<1, m->lanes, 0, m->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
 int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   if (!m || !st) return fail(LS_EINVAL, "null machine");
   ls_program* p = m->p;
   VMArgs a = make_args(m, max_steps);
-  if (!m->started) {
-    if (!a.refill) init_static_kernel<<<1, m->lanes, 0, m->stream>>>(a);
-    m->started = true;
-  }
+  m->started = true;
   const size_t smem = (p->blocks.size() + 1) * sizeof(int);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaMemsetAsync(m->flags + 1, 0, 2 * sizeof(int), m->stream));
