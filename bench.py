@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Headline benchmark: NUTS gradient evaluations / s on the B200 program-counter VM.
+
+Workload (BASELINE.json configs[1], the chain-count sweep's headline point):
+NUTS-lite on the 100-d equicorrelated gaussian (rho=0.5, target g100p500),
+max_tree_depth 10, step 0.25, 4 leapfrog steps per leaf, fp64, 2^16 chains
+per GPU, T iterations per step. A "step" runs the whole sampler program
+for every chain (all T iterations) — one pass of the hot path over one
+batch. Synthetic inputs: q0 = 0, unique per-chain keys.
+
+Metric unit: useful gradient evaluations, counted exactly as the reference
+does (sum over VM steps of active lanes x grad invocations in the block;
+reference metrics.py:68-76) — 2L per leaf per chain.
+
+Arms:
+  default            the B200 VM (this repo), chains sharded over ranks (weak scaling)
+  --impl reference   the reference's CPU algorithm (the oracle port of pc_vm.run),
+                     rank 0 only, on the host cores, bounded sample per step
+
+Timing: per step, CUDA events around the VM launch on the machine's stream
+(the library records them: ls_status.kernel_ms); W untimed warm-up steps;
+L2 flushed between timed steps; max over ranks. `e2e` times the public API
+call `paper_1910_11141_b200.run` with host arrays (H2D + D2H inside).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NUTS gradient evals/sec vs #chains at 1/2/4/8 B200 (+ % of roofline)"
+UNIT = "grad_evals/s"
+FP64_PEAK_FALLBACK = 37.0  # TFLOP/s, tools/fp64_peaks.cu on this pool's B200 (DFMA 36.9, DMMA 37.0)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--chains", type=int, default=1 << 16, help="chains per GPU")
+    ap.add_argument("--dim", type=int, default=100)
+    ap.add_argument("--iterations", type=int, default=10)
+    ap.add_argument("--depth", type=int, default=10)
+    ap.add_argument("--lanes", type=int, default=128, help="lanes per schedule group (CTA)")
+    ap.add_argument("--groups", type=int, default=0, help="persistent CTAs (0 = auto)")
+    ap.add_argument("--schedule", default="min_pc", choices=("min_pc", "most_populated"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-chains", type=int, default=256)
+    ap.add_argument("--cpu-iterations", type=int, default=10)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def program(args):
+    import paper_1910_11141_b200 as L
+
+    cfg = L.NutsConfig(step_size=0.25, leaf_steps=4, max_depth=args.depth,
+                       iterations=args.iterations, seed=0)
+    target = L.correlated_gaussian(args.dim, 0.5)
+    cp = L.compile_program(L.compile_source(L.nuts_lite_source(cfg, target), "nuts_main"))
+    return cfg, target, cp
+
+
+def chain_keys(first: int, count: int) -> np.ndarray:
+    """Unique per-chain keys (default_rng integers collide at 2^16+)."""
+    ids = np.arange(first, first + count, dtype=np.int64)
+    return (ids * 2654435761 + 12345) % (2**31 - 1)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(device), "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [r.split(", ") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip() == "Active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def flush_l2(torch, dev):
+    buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    torch.cuda.synchronize(dev)
+
+
+def measured_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(path))
+    except (OSError, ValueError):
+        return {}
+
+
+def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int):
+    """Time the oracle port of the reference pc engine (numpy masked mode) on host cores."""
+    import paper_1910_11141_b200 as L
+    from oracle import lockstep_oracle as O
+    from paper_1910_11141_b200.pc_vm import infer_types
+    from paper_1910_11141_b200.runtime import vtype_of
+
+    small = L.NutsConfig(step_size=cfg.step_size, leaf_steps=cfg.leaf_steps, max_depth=cfg.max_depth,
+                         iterations=iterations, seed=0)
+    scp = L.compile_program(L.compile_source(L.nuts_lite_source(small, target), "nuts_main"))
+    q0 = np.zeros((chains, target.dim))
+    key = chain_keys(0, chains)
+    types = infer_types(scp.flat, [vtype_of(q0), vtype_of(key)])
+    t0 = time.perf_counter()
+    res = O.run(scp, [q0, key], depth=small.min_stack_depth, types=types,
+                targets={target.name: target}, max_steps=None)
+    dt = time.perf_counter() - t0
+    grads = 0
+    for b, active in res.steps:
+        blk = scp.flat.blocks[b]
+        grads += active * sum(1 for op in blk.ops if getattr(op, "prim", None) is not None
+                              and op.prim.name == target.grad)
+    return grads, dt
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, target, cp = program(args)
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    for _ in range(args.warmup):
+        cpu_reference_sample(args, cfg, target, cp, min(args.cpu_chains, 64), args.cpu_iterations)
+    tot_g, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        g, dt = cpu_reference_sample(args, cfg, target, cp, args.cpu_chains, args.cpu_iterations)
+        tot_g += g
+        tot_t += dt
+    value = tot_g / tot_t
+    sample = (f"oracle port of reference pc_vm.run (numpy masked mode), {target.name}, "
+              f"{args.cpu_chains} chains x {args.cpu_iterations} iterations per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (q0=0, unique per-chain keys)",
+        "config": workload_config(args, target),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, target):
+    return {"workload": f"NUTS-lite on {args.dim}-d correlated gaussian (rho=0.5, {target.name})",
+            "chains_per_gpu": args.chains, "iterations": args.iterations, "max_tree_depth": args.depth,
+            "step_size": 0.25, "leaf_steps": 4, "precision": "fp64",
+            "lanes_per_group": args.lanes, "schedule": args.schedule,
+            "l2": "flushed between timed steps (256 MiB write); outputs exceed L2"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    import paper_1910_11141_b200 as L
+    from paper_1910_11141_b200 import _native
+    from paper_1910_11141_b200.lowering import lower
+    from paper_1910_11141_b200.pc_vm import infer_types
+    from paper_1910_11141_b200.runtime import vtype_of
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, target, cp = program(args)
+    z = args.chains
+    first = rank * z
+    q0 = np.zeros((z, args.dim))
+    key = chain_keys(first, z)
+    types = infer_types(cp.flat, [vtype_of(q0), vtype_of(key)])
+    dp = lower(cp, types, optimize=True)
+    prog = _native.Program(dp)
+    mach = _native.MachineHandle(prog, z, cfg.min_stack_depth, sched=args.schedule,
+                                 lanes_per_cta=args.lanes, ctas=args.groups, exact_logpdf=True)
+    # inputs resident in HBM before the timed region
+    q0_d = torch.zeros((z, args.dim), dtype=torch.float64, device=dev)
+    key_d = torch.from_numpy(key).to(dev)
+    mach.set_input_device(0, q0_d.data_ptr(), q0_d.numel() * 8)
+    mach.set_input_device(1, key_d.data_ptr(), key_d.numel() * 8)
+
+    def one_step():
+        mach.reset()
+        st = mach.run(-1)
+        if st.kind != _native.RUN_HALTED:
+            raise RuntimeError(f"VM did not halt: status {st.kind}")
+        return st
+
+    for _ in range(args.warmup):
+        one_step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    times, grads, launches0 = [], 0, None
+    for _ in range(args.steps):
+        flush_l2(torch, dev)
+        st = one_step()
+        if launches0 is None:
+            launches0 = st.launches - 1
+        times.append(st.kernel_ms)
+        grads += st.useful_grads
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    launches = st.launches - launches0
+    t_total = sum(times) / 1e3
+    if world > 1:
+        t = torch.tensor([t_total], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        g = torch.tensor([grads], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(g)
+        t_total, grads_all = float(t.item()), float(g.item())
+    else:
+        grads_all = float(grads)
+    value = grads_all / t_total
+    ms_per_step = 1e3 * t_total / args.steps
+
+    # roofline of the dominant kernel (vm_kernel: the whole step is one launch)
+    flops_per_grad = target.grad_flops
+    achieved = (grads / args.steps) * flops_per_grad / (np.mean(times) / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_FALLBACK, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_FALLBACK, "traffic": None,
+                "note": ("fp64 gradient FLOPs (2*d^2 per useful grad) / vm_kernel launch time; "
+                         "peak = measured fp64 DFMA/DMMA rate (tools/fp64_peaks.cu), MEASURED_PEAKS.json "
+                         "has no fp64 figure")}
+
+    # e2e through the public API with host buffers (H2D of inputs, D2H of chains inside)
+    e2e = None
+    if not args.no_e2e:
+        reps = max(1, min(args.steps, 2))
+        t0 = time.perf_counter()
+        g_e2e = 0
+        for _ in range(reps):
+            out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, lanes_per_group=args.lanes,
+                            groups=args.groups, schedule=args.schedule)
+            g_e2e += tr.useful_invocations({target.grad})
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+            gg = torch.tensor([g_e2e], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(gg)
+            g_e2e = float(gg.item())
+        e2e = {"value": g_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": int(q0.nbytes + key.nbytes),
+               "d2h_bytes_per_step": int(out.nbytes),
+               "path": "paper_1910_11141_b200.run(compiled, [q0, key]) with host numpy arrays"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g_cpu, dt_cpu = cpu_reference_sample(args, cfg, target, cp, args.cpu_chains, args.cpu_iterations)
+        cpu = {"value": g_cpu / dt_cpu, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+               "kind": "port",
+               "sample": (f"oracle port of reference pc_vm.run (numpy), {target.name}, "
+                          f"{args.cpu_chains} chains x {args.cpu_iterations} iterations, {dt_cpu:.1f}s")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (q0=0, unique per-chain keys, random-free target parameters)",
+            "config": {**workload_config(args, target), "parallelism": f"chains sharded over {world} GPU(s)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -164,6 +164,8 @@ typedef struct {
   int64_t steps;          /* steps executed so far (max over groups)           */
   int64_t useful_grads;   /* sum over steps of active lanes x grad invocations */
   int64_t launched_grads; /* sum over steps of group lanes x grad invocations  */
+  double kernel_ms;       /* CUDA-event time of this call's VM launch, on the machine's stream */
+  int64_t launches;       /* VM kernel launches issued by this machine so far  */
 } ls_status;
 
 typedef struct ls_program ls_program;
@@ -184,6 +186,8 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth,
                       const ls_machine_opts* opts, ls_machine** out);
 /* input `idx` of the program, host array of z * width words (lane-major) */
 int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes);
+/* rewind a machine to its freshly-seeded state (inputs kept), without reallocating */
+int ls_machine_reset(ls_machine* m);
 /* same, from device memory (e.g. a torch CUDA tensor) */
 int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes);
 /* Execute up to max_steps steps per group (<0: unbounded). Returns LS_OK and

@@ -42,7 +42,8 @@ class MachineOpts(C.Structure):
 class Status(C.Structure):
     _fields_ = [("kind", C.c_int32), ("var", C.c_int32), ("lane", C.c_int64),
                 ("block", C.c_int32), ("pad", C.c_int32), ("steps", C.c_int64),
-                ("useful_grads", C.c_int64), ("launched_grads", C.c_int64)]
+                ("useful_grads", C.c_int64), ("launched_grads", C.c_int64),
+                ("kernel_ms", C.c_double), ("launches", C.c_int64)]
 
 
 _lib = None
@@ -58,6 +59,7 @@ _SIGS = {
     "ls_machine_create": ([C.c_void_p, C.c_int64, C.c_int32, C.POINTER(MachineOpts),
                            C.POINTER(C.c_void_p)], C.c_int),
     "ls_machine_set_input": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
+    "ls_machine_reset": ([C.c_void_p], C.c_int),
     "ls_machine_set_input_device": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_run": ([C.c_void_p, C.c_int64, C.POINTER(Status)], C.c_int),
     "ls_read_output": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
@@ -172,6 +174,9 @@ class MachineHandle:
     def set_input(self, idx: int, arr: np.ndarray) -> None:
         arr = np.ascontiguousarray(arr)
         _check(load().ls_machine_set_input(self.handle, idx, _ptr(arr), arr.nbytes))
+
+    def reset(self) -> None:
+        _check(load().ls_machine_reset(self.handle))
 
     def set_input_device(self, idx: int, dev_ptr: int, nbytes: int) -> None:
         _check(load().ls_machine_set_input_device(self.handle, idx, C.c_void_p(dev_ptr), nbytes))

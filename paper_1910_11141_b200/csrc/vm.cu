@@ -697,6 +697,8 @@ struct ls_machine {
   int lane_trace_cap = 0;
   bool started = false;
   cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long launches = 0;
 };
 
 extern "C" {
@@ -786,6 +788,8 @@ int ls_machine_destroy(ls_machine* m) {
   cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
   cudaFree(m->blk_active); cudaFree(m->fault); cudaFree(m->flags);
   cudaFree(m->lane_trace); cudaFree(m->lane_trace_len);
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;
   return LS_OK;
@@ -918,6 +922,32 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   return LS_OK;
 }
 
+int ls_machine_reset(ls_machine* m) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  const size_t L = m->lanes, nb = m->p->blocks.size();
+  const int n_sp_rows = m->p->n_stacked + 1;
+  CK(cudaMemsetAsync(m->sp, 0, (size_t)m->groups * n_sp_rows * L * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->pcs, 0, (size_t)m->groups * (m->depth + 1) * L * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->counters, 0, 4 * sizeof(unsigned long long), m->stream));
+  CK(cudaMemsetAsync(m->group_steps, 0, m->groups * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->group_done, 0, m->groups * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->blk_steps, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->blk_active, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->flags, 0, 4 * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->trace_n, 0, sizeof(long long), m->stream));
+  if (m->lane_trace_len) CK(cudaMemsetAsync(m->lane_trace_len, 0, (size_t)m->z * sizeof(int), m->stream));
+  FaultRec f0{~0ull, 0, 0, 0, 0, -1};
+  CK(cudaMemcpyAsync(m->fault, &f0, sizeof(f0), cudaMemcpyHostToDevice, m->stream));
+  const bool refill = m->z > m->lanes;
+  std::vector<long long> slots((size_t)m->groups * L, -1);
+  if (!refill)
+    for (size_t t = 0; t < L; ++t) slots[t] = (long long)t < m->z ? (long long)t : -2;
+  CK(cudaMemcpyAsync(m->chain_of, slots.data(), slots.size() * sizeof(long long), cudaMemcpyHostToDevice, m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  m->started = false;
+  return static_init(m);
+}
+
 int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes) {
   if (!m || idx < 0 || idx >= (int)m->inputs.size()) return fail(LS_EINVAL, "bad input index");
   const int64_t want = m->z * m->input_width[idx] * 8;
@@ -992,9 +1022,18 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   const size_t smem = (p->blocks.size() + 1) * sizeof(int);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(vm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CK(cudaMemsetAsync(m->flags + 1, 0, 2 * sizeof(int), m->stream));
+  if (!m->ev0) {
+    CK(cudaEventCreate(&m->ev0));
+    CK(cudaEventCreate(&m->ev1));
+  }
+  CK(cudaEventRecord(m->ev0, m->stream));
   vm_kernel<<<m->groups, m->lanes, smem, m->stream>>>(a);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(m->ev1, m->stream));
   CK(cudaStreamSynchronize(m->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+  m->launches += 1;
   int flags[3];
   FaultRec f;
   std::vector<long long> gsteps(m->groups);
@@ -1007,6 +1046,8 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   CK(cudaMemcpy(cnt, m->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
   std::memset(st, 0, sizeof(*st));
   st->steps = *std::max_element(gsteps.begin(), gsteps.end());
+  st->kernel_ms = ms;
+  st->launches = m->launches;
   st->useful_grads = (int64_t)cnt[1];
   st->launched_grads = (int64_t)cnt[2];
   st->var = -1;
