@@ -133,6 +133,8 @@ typedef struct {
   int32_t kind;     /* LS_F64 / LS_I64 / LS_BOOL               */
   int32_t width;    /* words per lane (>= 1)                    */
   int32_t sp;       /* stack-pointer row for stacked vars, -1 otherwise */
+  int32_t row;      /* first workspace row (non-stacked vars; views may share rows) */
+  int32_t pad;
 } ls_var;
 
 typedef struct {
@@ -142,6 +144,7 @@ typedef struct {
   int32_t entry;
   const int32_t* inputs;  int32_t n_inputs;
   int32_t output;
+  int32_t flat_rows;      /* per-lane rows of all non-stacked storage (stacks follow) */
 } ls_program_desc;
 
 typedef struct {

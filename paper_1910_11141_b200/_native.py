@@ -30,7 +30,7 @@ class ProgramDesc(C.Structure):
                 ("vars", C.c_void_p), ("n_vars", C.c_int32),
                 ("entry", C.c_int32),
                 ("inputs", C.c_void_p), ("n_inputs", C.c_int32),
-                ("output", C.c_int32)]
+                ("output", C.c_int32), ("flat_rows", C.c_int32)]
 
 
 class MachineOpts(C.Structure):
@@ -129,7 +129,8 @@ class Program:
                       np.ascontiguousarray(dp.vars), np.ascontiguousarray(dp.inputs, dtype=np.int32)]
         b, o, v, i = self._keep
         desc = ProgramDesc(_ptr(b), len(b), _ptr(o) if len(o) else None, len(o), _ptr(v), len(v),
-                           dp.flat.entry, _ptr(i) if len(i) else None, len(i), dp.output)
+                           dp.flat.entry, _ptr(i) if len(i) else None, len(i), dp.output,
+                           dp.flat_rows)
         h = C.c_void_p()
         _check(lib.ls_program_create(C.byref(desc), C.byref(h)))
         self.handle = h

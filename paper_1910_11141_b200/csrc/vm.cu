@@ -655,6 +655,7 @@ struct ls_program {
   std::vector<int> inputs;
   int entry = 0, output = 0;
   int n_stacked = 0;
+  int flat_rows = 0;
   ls_block* d_blocks = nullptr;
   ls_op* d_ops = nullptr;
   ls_var* d_vars = nullptr;
@@ -727,6 +728,7 @@ int ls_program_create(const ls_program_desc* d, ls_program** out) {
   p->inputs.assign(d->inputs, d->inputs + d->n_inputs);
   p->entry = d->entry;
   p->output = d->output;
+  p->flat_rows = d->flat_rows;
   for (auto& v : p->vars) if (v.cls == LS_STACKED) p->n_stacked = std::max(p->n_stacked, v.sp + 1);
   for (auto& b : p->blocks) {
     if (b.op_begin < 0 || b.op_begin + b.op_count > d->n_ops) { delete p; return fail(LS_EINVAL, "block op range"); }
@@ -835,12 +837,20 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   const auto& vars = p->vars;
   m->var_row.resize(vars.size());
   m->var_depth.resize(vars.size());
-  int rows = 0;
+  int rows = p->flat_rows;  // non-stacked storage was laid out by the lowering
   for (size_t v = 0; v < vars.size(); ++v) {
     const int slots = vars[v].cls == LS_STACKED ? depth : 1;
-    m->var_row[v] = rows;
     m->var_depth[v] = slots;
-    rows += slots * vars[v].width;
+    if (vars[v].cls == LS_STACKED) {
+      m->var_row[v] = rows;
+      rows += slots * vars[v].width;
+    } else {
+      m->var_row[v] = vars[v].row;
+      if (vars[v].row < 0 || vars[v].row + vars[v].width > p->flat_rows) {
+        delete m;
+        return fail(LS_EINVAL, "variable rows outside the flat region");
+      }
+    }
   }
   m->group_rows = rows;
   m->out_width = vars[p->output].width;

@@ -40,8 +40,9 @@ OP_DTYPE = np.dtype([("opcode", "<i4"), ("action", "<i4"), ("out", "<i4"), ("nin
                      ("imm1", "<i4"), ("imm2", "<i4"), ("bits", "<i8")])
 BLOCK_DTYPE = np.dtype([("op_begin", "<i4"), ("op_count", "<i4"), ("term", "<i4"), ("a", "<i4"),
                         ("b", "<i4"), ("cond", "<i4"), ("grads", "<i4"), ("pad", "<i4")])
-VAR_DTYPE = np.dtype([("cls", "<i4"), ("kind", "<i4"), ("width", "<i4"), ("sp", "<i4")])
-assert OP_DTYPE.itemsize == 56 and BLOCK_DTYPE.itemsize == 32 and VAR_DTYPE.itemsize == 16
+VAR_DTYPE = np.dtype([("cls", "<i4"), ("kind", "<i4"), ("width", "<i4"), ("sp", "<i4"),
+                      ("row", "<i4"), ("pad", "<i4")])
+assert OP_DTYPE.itemsize == 56 and BLOCK_DTYPE.itemsize == 32 and VAR_DTYPE.itemsize == 24
 
 CLASS_CODE = {"stacked": 0, "register": 1, "temporary": 2}
 KIND_CODE = {"f64": 0, "i64": 1, "bool": 2}
@@ -174,6 +175,7 @@ class DeviceProgram:
     block_prims: list = field(default_factory=list)      # reference per-block prim counts
     block_stack_ops: list = field(default_factory=list)  # reference per-block stack ops
     optimized: bool = False
+    flat_rows: int = 0                                     # per-lane rows of non-stacked storage
 
 
 def _block_prims(flat: ir.FlatProgram) -> list[dict[str, int]]:
@@ -200,6 +202,158 @@ def _block_stack_ops(flat: ir.FlatProgram, classes: dict[str, str]) -> list[list
     return out
 
 
+def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict[str, str],
+             vtype, keep: set[str], optimize: bool):
+    """Assign every operand a device variable and every device variable its rows.
+
+    Returns (var list [(name, cls, VType, row)], renamed block_ops, renamed conds,
+    flat_rows). Rows of stacked variables are assigned by the C library after
+    the flat region (they depend on the machine's stack depth).
+
+    optimize=False: one device variable per program variable, private rows.
+    optimize=True: temporaries (block-local by construction, compiler.py:421-479)
+    are renamed per definition, then
+      * `T = id S` / `T = vslice:lo:hi S` with S at a static location that is not
+        rewritten while T lives becomes a zero-copy view of S's rows;
+      * `T = vcat(A, X)` where A (a temporary owning its rows) dies at this op
+        extends A in place (the VM skips the copy when dst == A);
+      * remaining temporaries share one per-lane arena by interval colouring.
+    """
+    entries: list[list] = []   # [name, cls, VType, row]
+    index: dict[str, int] = {}
+
+    def add(name, cls, vt, row=-1):
+        index[name] = len(entries)
+        entries.append([name, cls, vt, row])
+        return index[name]
+
+    flat_rows = 0
+    persistent = sorted(v for v, c in classes.items() if c != "temporary" or v in keep or not optimize)
+    for v in persistent:
+        cls = classes.get(v, "temporary")
+        vt = vtype(v)
+        if cls == "stacked":
+            add(v, cls, vt)
+        else:
+            add(v, cls, vt, flat_rows)
+            flat_rows += vt.words
+    if not optimize:
+        renamed = [[dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]]) for op in ops]
+                   for ops in block_ops]
+        return entries, renamed, [index[c] if c else 0 for c in conds], flat_rows
+
+    is_temp = {v for v, c in classes.items() if c == "temporary" and v not in keep}
+    arena_base = flat_rows
+    arena_size = 0
+    new_blocks, new_conds = [], []
+    for bi, ops in enumerate(block_ops):
+        # --- SSA-rename temporaries of this block
+        cur: dict[str, str] = {}
+        inst: dict[str, dict] = {}   # instance -> info
+        renamed = []
+        for k, op in enumerate(ops):
+            ins = [cur.get(i, i) for i in op["ins"]]
+            for i in ins:
+                if i in inst:
+                    inst[i]["end"] = max(inst[i]["end"], k)
+            out = op["out"]
+            if out in is_temp and op["action"] != ACTION_POP:
+                name = f"{out}@{bi}.{k}"
+                cur[out] = name
+                inst[name] = {"start": k, "end": k, "vt": vtype(out), "op": k}
+                out = name
+            renamed.append(dict(op, out=out, ins=ins))
+        cond = conds[bi]
+        if cond is not None:
+            cond = cur.get(cond, cond)
+            if cond in inst:
+                inst[cond]["end"] = max(inst[cond]["end"], len(ops))
+
+        # registers written inside this block, by op position
+        writes: dict[str, list[int]] = {}
+        for k, op in enumerate(renamed):
+            if op["out"] not in inst:
+                writes.setdefault(op["out"], []).append(k)
+
+        def stable(src: str, a: int, b: int) -> bool:
+            """src keeps its value and location over ops (a, b]."""
+            if src in inst:
+                return True
+            if classes.get(src) != "register" and src not in keep:
+                return False
+            return not any(a < w <= b for w in writes.get(src, ()))
+
+        # --- views and in-place vcat chains
+        owner: dict[str, tuple[str, int]] = {}   # instance -> (root owner, word offset)
+
+        def root(n):
+            return owner.get(n, (n, 0))
+
+        for name, info in sorted(inst.items(), key=lambda kv: kv[1]["start"]):
+            op = renamed[info["op"]]
+            prim, end = op["prim"], info["end"]
+            if prim == "id" or prim.startswith("vslice:"):
+                src = op["ins"][0]
+                lo = int(prim.split(":")[1]) if prim != "id" else 0
+                if (src in inst or classes.get(src) == "register" or src in keep) \
+                        and classes.get(src) != "stacked" and stable(src, info["start"], end):
+                    r, off = root(src)
+                    owner[name] = (r, off + lo)
+                    if r in inst:
+                        inst[r]["end"] = max(inst[r]["end"], end)
+            elif prim == "vcat":
+                a = op["ins"][0]
+                if a in inst and a not in owner and inst[a]["end"] == info["start"] \
+                        and op["ins"][1] != a and root(op["ins"][1])[0] != a:
+                    owner[name] = (a, 0)
+                    inst[a]["end"] = max(inst[a]["end"], end)
+                    inst[a]["span"] = max(inst[a].get("span", inst[a]["vt"].words), info["vt"].words)
+        # the storage owner of every view / chain member must outlive it
+        for name in owner:
+            r = name
+            while r in owner:
+                r = owner[r][0]
+            if r in inst:
+                inst[r]["end"] = max(inst[r]["end"], inst[name]["end"])
+
+        # --- arena allocation (first fit by start, closed intervals)
+        live: list[tuple[int, int, int]] = []  # (end, offset, size)
+        top = 0
+        placed: dict[str, int] = {}
+        for name, info in sorted(inst.items(), key=lambda kv: (kv[1]["start"], kv[0])):
+            if name in owner:
+                continue
+            size = info.get("span", info["vt"].words)
+            live = [x for x in live if x[0] >= info["start"]]
+            off, ok = 0, False
+            for cand in sorted({0} | {o + s for _, o, s in live}):
+                if all(cand + size <= o or cand >= o + s for _, o, s in live):
+                    off, ok = cand, True
+                    break
+            assert ok
+            placed[name] = off
+            live.append((info["end"], off, size))
+            top = max(top, off + size)
+        arena_size = max(arena_size, top)
+
+        def final_row(n):
+            r, off = n, 0
+            while r in owner:
+                r2, o2 = owner[r]
+                off += o2
+                r = r2
+            if r in placed:
+                return arena_base + placed[r] + off
+            return entries[index[r]][3] + off
+
+        for name, info in inst.items():
+            add(name, "temporary", info["vt"], final_row(name))
+        new_blocks.append([dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]])
+                           for op in renamed])
+        new_conds.append(index[cond] if cond is not None else 0)
+    return entries, new_blocks, new_conds, arena_base + arena_size
+
+
 def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool = True) -> DeviceProgram:
     """Build the device tables for `compiled` given inferred lane types."""
     flat, classes = compiled.flat, dict(compiled.classes)
@@ -208,34 +362,25 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
         flat = fuse_copies(flat, classes)
 
     grads = grad_names()
-    names = sorted(set(classes) | set(types))
-    for n in names:
+    for n in set(types):
         classes.setdefault(n, "temporary")
-    index = {n: i for i, n in enumerate(names)}
-    scratch_count = [0]
+    extra_types: dict[str, VType] = {}
 
     def vtype(v: str) -> VType:
-        return types.get(v, VType("i64"))
-
-    extra_vars: list[tuple[str, VType]] = []
-
-    def scratch_for(vt: VType) -> int:
-        name = f"$scratch{scratch_count[0]}"
-        scratch_count[0] += 1
-        extra_vars.append((name, vt))
-        index[name] = len(names) + len(extra_vars) - 1
-        return index[name]
+        return extra_types.get(v) or types.get(v, VType("i64"))
 
     targets: list = []
-    op_rows: list[tuple] = []
-    block_rows = []
     ref_prims = _block_prims(compiled.flat)
-
+    block_ops: list[list[dict]] = []
+    conds: list[str | None] = []
+    terms = []
+    n_scratch = 0
     for bi, blk in enumerate(flat.blocks):
-        begin = len(op_rows)
+        ops: list[dict] = []
         for op in blk.ops:
             if isinstance(op, ir.Pop):
-                op_rows.append((0, ACTION_POP, index[op.var], 0, [0, 0, 0], 0, 1, 0, 0, 0, 0))
+                ops.append(dict(opcode=0, action=ACTION_POP, out=op.var, ins=[], kind=0, width=1,
+                                imm0=0, imm1=0, imm2=0, bits=0, prim="$pop"))
                 continue
             k = resolve_kernel(op.prim.name)
             if k.device is None:
@@ -247,55 +392,72 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             in_kind = KIND_CODE[vtype(op.inputs[0]).kind] if op.inputs else KIND_CODE[out_vt.kind]
             imm0, imm1, bits = dev.imm0, dev.imm1, 0
             if dev.opcode == OPCODES["const"]:
-                bits = dev.imm0
-                imm0 = 0
+                bits, imm0 = dev.imm0, 0
             if dev.target is not None:
                 if dev.target not in targets:
                     targets.append(dev.target)
                 imm0 = targets.index(dev.target)
             action = ACTION_PUSH if isinstance(op, ir.Push) else ACTION_UPDATE
-            ins = [index[v] for v in op.inputs]
-            row = [dev.opcode, action, index[op.output], len(ins), ins + [0] * (3 - len(ins)),
-                   in_kind, out_vt.words, imm0, imm1, 0, bits]
-            hazard = (action == ACTION_UPDATE and op.output in op.inputs
-                      and not _inplace_safe(op, op.output))
-            if hazard:
-                tmp = scratch_for(out_vt)
-                row[2] = tmp
-                op_rows.append(tuple(row))
-                op_rows.append((OPCODES["id"], ACTION_UPDATE, index[op.output], 1, [tmp, 0, 0],
-                                KIND_CODE[out_vt.kind], out_vt.words, 0, 0, 0, 0))
+            row = dict(opcode=dev.opcode, action=action, out=op.output, ins=list(op.inputs),
+                       kind=in_kind, width=out_vt.words, imm0=imm0, imm1=imm1, imm2=0, bits=bits,
+                       prim=op.prim.name)
+            if action == ACTION_UPDATE and op.output in op.inputs and not _inplace_safe(op, op.output):
+                tmp = f"$scratch{n_scratch}"
+                n_scratch += 1
+                extra_types[tmp] = out_vt
+                classes[tmp] = "temporary"
+                ops.append(dict(row, out=tmp))
+                ops.append(dict(opcode=OPCODES["id"], action=ACTION_UPDATE, out=op.output, ins=[tmp],
+                                kind=KIND_CODE[out_vt.kind], width=out_vt.words, imm0=0, imm1=0,
+                                imm2=0, bits=0, prim="id"))
             else:
-                op_rows.append(tuple(row))
+                ops.append(row)
         t = blk.terminator
         if isinstance(t, ir.FlatJump):
-            term = (TERM_JUMP, t.target, 0, 0)
+            terms.append((TERM_JUMP, t.target, 0))
+            conds.append(None)
         elif isinstance(t, ir.FlatBranch):
-            term = (TERM_BRANCH, t.true_target, t.false_target, index[t.cond])
+            terms.append((TERM_BRANCH, t.true_target, t.false_target))
+            conds.append(t.cond)
         elif isinstance(t, ir.PushJump):
-            term = (TERM_PUSHJUMP, t.jump_to, t.return_to, 0)
+            terms.append((TERM_PUSHJUMP, t.jump_to, t.return_to))
+            conds.append(None)
         else:
-            term = (TERM_RETURN, 0, 0, 0)
-        g = sum(n for name, n in ref_prims[bi].items() if name in grads)
-        block_rows.append((begin, len(op_rows) - begin, term[0], term[1], term[2], term[3], g, 0))
+            terms.append((TERM_RETURN, 0, 0))
+            conds.append(None)
+        block_ops.append(ops)
 
-    all_names = names + [n for n, _ in extra_vars]
-    all_types = {**{n: vtype(n) for n in names}, **dict(extra_vars)}
-    var_arr = np.zeros(len(all_names), dtype=VAR_DTYPE)
+    keep = set(flat.inputs) | {flat.output}
+    entries, dev_blocks, dev_conds, flat_rows = _storage(block_ops, conds, classes, vtype, keep, optimize)
+
+    op_rows, block_rows = [], []
+    for bi, ops in enumerate(dev_blocks):
+        begin = len(op_rows)
+        for op in ops:
+            ins = op["ins"] + [0] * (3 - len(op["ins"]))
+            op_rows.append((op["opcode"], op["action"], op["out"], len(op["ins"]), ins, op["kind"],
+                            op["width"], op["imm0"], op["imm1"], op["imm2"], op["bits"]))
+        g = sum(n for name, n in ref_prims[bi].items() if name in grads)
+        tt = terms[bi]
+        block_rows.append((begin, len(op_rows) - begin, tt[0], tt[1], tt[2], dev_conds[bi], g, 0))
+
+    var_arr = np.zeros(len(entries), dtype=VAR_DTYPE)
     sp_row = 0
-    for i, n in enumerate(all_names):
-        vt = all_types[n]
-        cls = classes.get(n, "temporary")
-        var_arr[i] = (CLASS_CODE[cls], KIND_CODE[vt.kind], vt.words, sp_row if cls == "stacked" else -1)
+    for i, (name, cls, vt, row) in enumerate(entries):
+        var_arr[i] = (CLASS_CODE[cls], KIND_CODE[vt.kind], vt.words,
+                      sp_row if cls == "stacked" else -1, row, 0)
         if cls == "stacked":
             sp_row += 1
-    ops = np.zeros(len(op_rows), dtype=OP_DTYPE)
+    ops_arr = np.zeros(len(op_rows), dtype=OP_DTYPE)
     for i, r in enumerate(op_rows):
-        ops[i] = r
+        ops_arr[i] = r
     blocks = np.array(block_rows, dtype=BLOCK_DTYPE) if block_rows else np.zeros(0, BLOCK_DTYPE)
+    names = [e[0] for e in entries]
+    index = {n: i for i, n in enumerate(names)}
     return DeviceProgram(
-        compiled=compiled, flat=flat, classes=classes, types=all_types, var_names=all_names,
-        var_index={n: i for i, n in enumerate(all_names)}, blocks=blocks, ops=ops, vars=var_arr,
-        inputs=np.array([index[v] for v in flat.inputs], dtype=np.int32),
+        compiled=compiled, flat=flat, classes={e[0]: e[1] for e in entries},
+        types={e[0]: e[2] for e in entries}, var_names=names, var_index=index, blocks=blocks,
+        ops=ops_arr, vars=var_arr, inputs=np.array([index[v] for v in flat.inputs], dtype=np.int32),
         output=index[flat.output], targets=targets, block_prims=ref_prims,
-        block_stack_ops=_block_stack_ops(compiled.flat, compiled.classes), optimized=optimize)
+        block_stack_ops=_block_stack_ops(compiled.flat, compiled.classes), optimized=optimize,
+        flat_rows=flat_rows)

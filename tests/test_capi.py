@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_struct_layouts_match_header():
-    assert OP_DTYPE.itemsize == 56 and BLOCK_DTYPE.itemsize == 32 and VAR_DTYPE.itemsize == 16
+    assert OP_DTYPE.itemsize == 56 and BLOCK_DTYPE.itemsize == 32 and VAR_DTYPE.itemsize == 24
     assert C.sizeof(_native.Status) == 64
     assert C.sizeof(_native.MachineOpts) == 32
 

@@ -80,3 +80,43 @@ def test_block_tables_keep_reference_numbering():
         t_ = blk.terminator
         if isinstance(t_, ir.PushJump):
             assert (dp.blocks[bi]["a"], dp.blocks[bi]["b"]) == (t_.jump_to, t_.return_to)
+
+
+def _sim_matches_oracle(cp, ins, depth, opt):
+    from oracle import table_sim
+
+    types = infer_types(cp.flat, [vtype_of(a) for a in ins])
+    dp = lower(cp, types, optimize=opt)
+    out, traces = table_sim.run(dp, ins, depth)
+    ref = oracle_run(cp, ins, depth, lane_traces=True)
+    want = ref.output.astype(np.uint64) if ref.output.dtype == np.bool_ else ref.output
+    want = np.ascontiguousarray(want).view(np.uint64).reshape(out.shape)
+    if ref.output.dtype.kind == "f":
+        np.testing.assert_allclose(out.view(np.float64), want.view(np.float64), rtol=1e-12, atol=1e-15)
+    else:
+        assert np.array_equal(out, want)
+    assert all(a == b for a, b in zip(traces, ref.lane_blocks))
+    return dp
+
+
+def test_device_tables_simulate_to_oracle_results(corpus_compiled):
+    """Storage assignment (arena, views, in-place vcat, demotion) preserves every lane's result."""
+    import itertools
+
+    from paper_1910_11141_b200.compiler import CompileOptions
+
+    rng = np.random.default_rng(3)
+    for name, (e, cfg, _) in corpus_compiled.items():
+        for bits in itertools.product([True, False], repeat=4):
+            cp = L.compile_program(cfg, CompileOptions(*bits))
+            ins = e.make_inputs(rng, 3)
+            for opt in (False, True):
+                _sim_matches_oracle(cp, ins, 64, opt)
+
+
+def test_nuts_tables_shrink_and_stay_exact():
+    cfg, t, cp = nuts_program({"dim": 100, "rho": 0.5, "config": dict(max_depth=10, iterations=3)})
+    ins = [np.zeros((2, 100)), np.array([5, 6], np.int64)]
+    plain = _sim_matches_oracle(cp, ins, cfg.min_stack_depth, False)
+    opt = _sim_matches_oracle(cp, ins, cfg.min_stack_depth, True)
+    assert opt.flat_rows * 5 < plain.flat_rows
