@@ -155,7 +155,10 @@ typedef struct {
   int32_t trace;          /* record (block, active) per step (single group only)      */
   int32_t exact_logpdf;   /* 1: numpy einsum summation order; 0: fused fast form      */
   int32_t lane_trace_cap; /* >0: record each chain's block sequence (first cap steps) */
-  int32_t reserved[2];
+  int32_t warp_groups;    /* 1: throughput engine — every warp is a 32-lane group with
+                             DMMA target contractions and fused superblocks; `ctas`
+                             then counts CTAs of 4 warps */
+  int32_t reserved[1];
 } ls_machine_opts;
 
 typedef struct {

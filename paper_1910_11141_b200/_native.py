@@ -36,7 +36,7 @@ class ProgramDesc(C.Structure):
 class MachineOpts(C.Structure):
     _fields_ = [("sched", C.c_int32), ("lanes_per_cta", C.c_int32), ("ctas", C.c_int32),
                 ("trace", C.c_int32), ("exact_logpdf", C.c_int32), ("lane_trace_cap", C.c_int32),
-                ("reserved", C.c_int32 * 2)]
+                ("warp_groups", C.c_int32), ("reserved", C.c_int32 * 1)]
 
 
 class Status(C.Structure):
@@ -158,7 +158,7 @@ class MachineHandle:
 
     def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
                  lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
-                 exact_logpdf: bool = True, lane_trace_cap: int = 0):
+                 exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False):
         lib = load()
         if sched not in SCHED:
             raise ValueError(f"unknown schedule '{sched}'")
@@ -166,7 +166,7 @@ class MachineHandle:
         self.z = z
         self.depth = depth
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
-                           int(lane_trace_cap))
+                           int(lane_trace_cap), int(warp_groups))
         self.lane_trace_cap = int(lane_trace_cap)
         h = C.c_void_p()
         _check(lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)))

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "liblockstep_b200.so"
-SOURCES = [CSRC / "vm.cu"]
+SOURCES = [CSRC / "engine.cu"]
 DEPS = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "lockstep_b200.h"]
 
 NVCC_FLAGS = [

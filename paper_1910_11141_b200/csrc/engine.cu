@@ -1,0 +1,999 @@
+// engine.cu — the B200 program-counter VM (paper Alg. 2 / reference pc_vm.py) and its C ABI.
+//
+// Two engines share the per-lane semantics of lsb_vm.cuh (exec_block):
+//
+//   vm_cta_kernel  — "exact" / "cta": one CTA is one autobatching group of up
+//                    to 1024 lanes (one thread per lane). Each step the CTA
+//                    reduces its live lanes' program counters (warp min /
+//                    __match_any_sync histogram + shared-memory combine),
+//                    selects one block, and the threads at that block run it.
+//                    With one group this reproduces the reference's global
+//                    min-pc schedule step for step (pc_vm.py:304-332).
+//   vm_warp_kernel — "warp": the throughput engine. Every warp is its own
+//                    32-lane group scheduled by warp votes, with no CTA
+//                    barriers; target gradients run warp-cooperatively on the
+//                    fp64 tensor pipe (DMMA) and recognised leapfrog functions
+//                    run as fused superblocks. Lanes refill from a chain queue.
+//
+// Both kernels are persistent and resumable: all machine state lives in HBM
+// (per-group workspaces), so a launch may stop after any step. Faults are
+// reported as the lowest (op position, lane) of the faulting step like
+// reference runtime.py:462-507, and stop the machine (no rollback).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lockstep_b200.h"
+#include "lsb_vm.cuh"
+
+using namespace lsbvm;
+using lsb::as_f64;
+using lsb::f64_bits;
+
+namespace {
+
+struct CtaShared {
+  int pick;
+  int count;
+  unsigned long long fault_key;
+  int warp_val[kMaxLanes / 32];
+  int warp_cnt[kMaxLanes / 32];
+};
+
+__global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant__ VMArgs a) {
+  extern __shared__ int s_hist[];  // [n_blocks + 1]
+  __shared__ CtaShared sh;
+  const int g = blockIdx.x;
+  const int t = threadIdx.x;
+  const int L = a.lanes;
+  const int lane_id = t & 31, warp = t >> 5, nwarps = (L + 31) >> 5;
+  const Lane ln{a.ws + (size_t)g * a.group_rows * L, a.sp + (size_t)g * a.n_sp_rows * L,
+                a.pcs + (size_t)g * (a.depth + 1) * L, t, L};
+  int* pc_sp = &ln.sp_row(a.n_sp_rows - 1);
+  long long* my_chain = a.chain_of + (size_t)g * L + t;
+  long long steps = a.group_steps[g];
+  long long* bsteps = a.blk_steps + (size_t)g * a.n_blocks;
+  long long* bactive = a.blk_active + (size_t)g * a.n_blocks;
+  unsigned long long useful = 0, launched = 0;
+  if (a.group_done[g]) return;
+
+  for (;;) {
+    if (a.refill && *my_chain == -1) {
+      const unsigned long long c = atomicAdd(a.next_chain, 1ull);
+      if ((long long)c < a.z) {
+        *my_chain = (long long)c;
+        init_lane(a, ln, (long long)c);
+      } else {
+        *my_chain = -2;
+      }
+    }
+    const int pc = *my_chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + t] : a.halt;
+    if (t == 0) sh.fault_key = ~0ull;
+    if (a.sched == LS_SCHED_MOST_POPULATED) {
+      for (int b = t; b <= a.n_blocks; b += L) s_hist[b] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(kFull, pc);
+      if (pc != a.halt && lane_id == __ffs(peers) - 1) atomicAdd(&s_hist[pc], __popc(peers));
+      __syncthreads();
+      int best = -1, best_b = a.halt;
+      for (int b = t; b < a.n_blocks; b += L) {
+        const int c = s_hist[b];
+        if (c > best) { best = c; best_b = b; }
+      }
+      unsigned long long key = best > 0 ? (((unsigned long long)(unsigned)best) << 32) |
+                                              (unsigned)(0x7fffffff - best_b) : 0ull;
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(kFull, key, o);
+        key = other > key ? other : key;
+      }
+      if (lane_id == 0) {
+        sh.warp_val[warp] = (int)(key >> 32);
+        sh.warp_cnt[warp] = (int)(0x7fffffff - (int)(key & 0xffffffffu));
+      }
+      __syncthreads();
+      if (t == 0) {
+        int bc = 0, bb = a.halt;
+        for (int w2 = 0; w2 < nwarps; ++w2) {
+          const int c = sh.warp_val[w2], b = sh.warp_cnt[w2];
+          if (c > bc || (c == bc && c > 0 && b < bb)) { bc = c; bb = b; }
+        }
+        sh.pick = bc > 0 ? bb : a.halt;
+        sh.count = bc;
+      }
+      __syncthreads();
+    } else {
+      const int m = __reduce_min_sync(kFull, (unsigned)pc);
+      if (lane_id == 0) sh.warp_val[warp] = m;
+      __syncthreads();
+      if (t == 0) {
+        int mm = a.halt;
+        for (int w2 = 0; w2 < nwarps; ++w2) mm = min(mm, sh.warp_val[w2]);
+        sh.pick = mm;
+      }
+      __syncthreads();
+      const unsigned bal = __ballot_sync(kFull, pc == sh.pick && pc != a.halt);
+      if (lane_id == 0) sh.warp_cnt[warp] = __popc(bal);
+      __syncthreads();
+      if (t == 0) {
+        int c = 0;
+        for (int w2 = 0; w2 < nwarps; ++w2) c += sh.warp_cnt[w2];
+        sh.count = c;
+      }
+      __syncthreads();
+    }
+    const int b = sh.pick;
+    if (b == a.halt) {
+      if (t == 0) a.group_done[g] = 1;
+      break;
+    }
+    if (*(volatile int*)a.abort_flag) break;
+    if (a.max_steps >= 0 && steps >= a.max_steps) {
+      if (t == 0) a.paused[0] = 1;
+      break;
+    }
+    if (a.trace_block != nullptr && *a.trace_n >= a.trace_cap) {  // host drains and resumes
+      if (t == 0) a.paused[1] = 1;
+      break;
+    }
+    const bool active = pc == b;
+    if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
+    StepFault f;
+    const bool halted_now = exec_block<false>(a, ln, b, active, *my_chain, f, nullptr);
+    if (f.pos) atomicMin(&sh.fault_key, ((unsigned long long)(f.pos - 1) << 32) | (unsigned)t);
+    __syncthreads();
+    if (sh.fault_key != ~0ull) {
+      if ((unsigned)(sh.fault_key & 0xffffffffu) == (unsigned)t && f.pos &&
+          (unsigned)(f.pos - 1) == (unsigned)(sh.fault_key >> 32)) {
+        a.fault->key = sh.fault_key;
+        a.fault->kind = f.kind;
+        a.fault->var = f.var;
+        a.fault->block = b;
+        a.fault->detail = f.detail;
+        a.fault->chain = *my_chain;
+        __threadfence();
+        atomicExch(a.abort_flag, 1);
+      }
+      steps++;
+      break;
+    }
+    if (halted_now) {
+      write_output(a, ln, *my_chain);
+      if (a.refill) *my_chain = -1;
+    }
+    if (t == 0) {
+      if (a.trace_block != nullptr) {
+        const long long n = *a.trace_n;
+        a.trace_block[n] = b;
+        a.trace_active[n] = sh.count;
+        *a.trace_n = n + 1;
+      }
+      const int grads = a.blocks[b].grads;
+      bsteps[b] += 1;
+      bactive[b] += sh.count;
+      useful += (unsigned long long)sh.count * (unsigned long long)grads;
+      launched += (unsigned long long)L * (unsigned long long)grads;
+    }
+    ++steps;
+    __syncthreads();
+  }
+  if (t == 0) {
+    a.group_steps[g] = steps;
+    if (useful) atomicAdd(a.useful, useful);
+    if (launched) atomicAdd(a.launched, launched);
+  }
+}
+
+__global__ void __launch_bounds__(128, 4) vm_warp_kernel(const __grid_constant__ VMArgs a) {
+  extern __shared__ double lf_smem[];
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= a.n_groups) return;
+  constexpr int L = 32;
+  const Lane ln{a.ws + (size_t)g * a.group_rows * L, a.sp + (size_t)g * a.n_sp_rows * L,
+                a.pcs + (size_t)g * (a.depth + 1) * L, lane, L};
+  double* my_smem = lf_smem + (size_t)(threadIdx.x >> 5) * a.lf_smem_per_warp;
+  int* pc_sp = &ln.sp_row(a.n_sp_rows - 1);
+  long long* my_chain = a.chain_of + (size_t)g * L + lane;
+  long long steps = a.group_steps[g];
+  long long* bsteps = a.blk_steps + (size_t)g * a.n_blocks;
+  long long* bactive = a.blk_active + (size_t)g * a.n_blocks;
+  unsigned long long useful = 0, launched = 0;
+  if (a.group_done[g]) return;
+
+  for (;;) {
+    if (*my_chain == -1) {
+      const unsigned long long c = atomicAdd(a.next_chain, 1ull);
+      if ((long long)c < a.z) {
+        *my_chain = (long long)c;
+        init_lane(a, ln, (long long)c);
+      } else {
+        *my_chain = -2;
+      }
+    }
+    const int pc = *my_chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + lane] : a.halt;
+    int b;
+    if (a.sched == LS_SCHED_MOST_POPULATED) {
+      const unsigned peers = __match_any_sync(kFull, pc);
+      const unsigned key = pc == a.halt ? 0u : ((unsigned)__popc(peers) << 16) | (0xffffu - (unsigned)pc);
+      const unsigned best = __reduce_max_sync(kFull, key);
+      b = best == 0 ? a.halt : (int)(0xffffu - (best & 0xffffu));
+    } else {
+      b = (int)__reduce_min_sync(kFull, (unsigned)pc);
+    }
+    if (b == a.halt) {
+      if (lane == 0) a.group_done[g] = 1;
+      break;
+    }
+    if (*(volatile int*)a.abort_flag) break;
+    if (a.max_steps >= 0 && steps >= a.max_steps) {
+      if (lane == 0) a.paused[0] = 1;
+      break;
+    }
+    const bool active = pc == b;
+    const int count = __popc(__ballot_sync(kFull, active));
+    if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
+    StepFault f;
+    const bool halted_now = exec_block<true>(a, ln, b, active, *my_chain, f, my_smem);
+    const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
+    const unsigned wmin = __reduce_min_sync(kFull, fkey);
+    if (wmin != ~0u) {
+      if (fkey == wmin) {
+        // several groups may fault in one launch: the lowest chain is reported
+        const unsigned long long key = (unsigned long long)(*my_chain);
+        const unsigned long long old = atomicMin(&a.fault->key, key);
+        if (key < old) {
+          a.fault->kind = f.kind;
+          a.fault->var = f.var;
+          a.fault->block = b;
+          a.fault->detail = f.detail;
+          a.fault->chain = *my_chain;
+        }
+        __threadfence();
+        atomicExch(a.abort_flag, 1);
+      }
+      ++steps;
+      break;
+    }
+    if (halted_now) {
+      write_output(a, ln, *my_chain);
+      *my_chain = -1;
+    }
+    if (lane == 0) {
+      const int grads = a.blocks[b].grads;
+      bsteps[b] += 1;
+      bactive[b] += count;
+      useful += (unsigned long long)count * (unsigned long long)grads;
+      launched += (unsigned long long)L * (unsigned long long)grads;
+    }
+    ++steps;
+  }
+  if (lane == 0) {
+    a.group_steps[g] = steps;
+    if (useful) atomicAdd(a.useful, useful);
+    if (launched) atomicAdd(a.launched, launched);
+  }
+}
+
+__global__ void init_static_kernel(const __grid_constant__ VMArgs a) {
+  const int t = threadIdx.x;
+  const long long c = a.chain_of[t];
+  if (c < 0) return;
+  const Lane ln{a.ws, a.sp, a.pcs, t, a.lanes};
+  init_lane(a, ln, c);
+}
+
+__global__ void rng_kernel(const int64_t* key, const int64_t* ctr, long long n, double* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = lsb::rng_uniform(key[i], ctr[i]);
+}
+
+__global__ void target_eval_kernel(DevTarget tg, int which, const double* x, long long z, double* out,
+                                   uint64_t* scratch) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= z) return;
+  const int d = tg.dim;
+  uint64_t* xs = scratch + i;  // lane-minor copy, stride z
+  for (int j = 0; j < d; ++j) xs[(size_t)j * z] = f64_bits(x[(size_t)i * d + j]);
+  if (which == 0) {
+    out[i] = target_logpdf(tg, xs, (int)z, 1);
+  } else {
+    uint64_t* gs = scratch + (size_t)d * z + i;
+    target_grad(tg, xs, (int)z, gs);
+    for (int j = 0; j < d; ++j) out[(size_t)i * d + j] = as_f64(gs[(size_t)j * z]);
+  }
+}
+
+}  // namespace
+
+// =====================================================================================
+// Host side: C ABI
+// =====================================================================================
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                                    \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) return fail(LS_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+static int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) return fail(LS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  return LS_OK;
+}
+
+template <class T>
+static int upload(T** d, const std::vector<T>& h) {
+  int rc = dalloc(d, h.size());
+  if (rc) return rc;
+  if (!h.empty()) CK(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
+struct ls_program {
+  std::vector<ls_block> blocks;
+  std::vector<ls_op> ops;
+  std::vector<ls_var> vars;
+  std::vector<int> inputs;
+  int entry = 0, output = 0;
+  int n_stacked = 0;
+  int flat_rows = 0;
+  DevTarget targets[kMaxTargets];
+  std::vector<double*> owned;
+};
+
+struct ls_machine {
+  ls_program* p = nullptr;
+  long long z = 0;
+  int depth = 0, lanes = 0, groups = 0, group_rows = 0;
+  ls_machine_opts opts{};
+  std::vector<int> var_row, var_depth, input_width, input_rows;
+  RBlock* d_blocks = nullptr;
+  ROp* d_ops = nullptr;
+  int* d_input_width = nullptr;
+  int* d_input_rows = nullptr;
+  uint64_t* ws = nullptr;
+  int* sp = nullptr;
+  int* pcs = nullptr;
+  long long* chain_of = nullptr;
+  std::vector<uint64_t*> inputs;
+  uint64_t** d_input_ptrs = nullptr;
+  uint64_t* output = nullptr;
+  int out_width = 0;
+  unsigned long long* counters = nullptr;  // [0] next_chain [1] useful [2] launched
+  long long* group_steps = nullptr;
+  int* group_done = nullptr;
+  int* trace_block = nullptr;
+  int* trace_active = nullptr;
+  long long trace_cap = 0;
+  long long* trace_n = nullptr;
+  long long* blk_steps = nullptr;
+  long long* blk_active = nullptr;
+  FaultRec* fault = nullptr;
+  int* flags = nullptr;  // [0] abort [1] paused-steps [2] paused-trace
+  int* lane_trace = nullptr;
+  int* lane_trace_len = nullptr;
+  int lane_trace_cap = 0;
+  bool started = false;
+  bool warp = false;
+  bool refill = false;
+  int lf_smem_per_warp = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long launches = 0;
+};
+
+static int static_init(ls_machine* m);
+
+// Resolve program ops/blocks against this machine's storage layout (lsb_vm.cuh ROp).
+static void resolve(const ls_machine* m, std::vector<ROp>& rops, std::vector<RBlock>& rblocks) {
+  const ls_program* p = m->p;
+  auto row_of = [&](int v) { return m->var_row[v]; };
+  auto sp_of = [&](int v) { return p->vars[v].cls == LS_STACKED ? p->vars[v].sp : -1; };
+  rops.resize(p->ops.size());
+  for (size_t i = 0; i < p->ops.size(); ++i) {
+    const ls_op& o = p->ops[i];
+    ROp r{};
+    r.opcode = o.opcode; r.action = o.action; r.nin = o.nin; r.kind = o.kind;
+    r.width = o.width; r.out = o.out; r.out_row = row_of(o.out); r.out_sp = sp_of(o.out);
+    for (int j = 0; j < 3; ++j) {
+      if (j < o.nin) {
+        const int v = o.in[j];
+        r.in_row[j] = row_of(v); r.in_sp[j] = sp_of(v); r.in_w[j] = p->vars[v].width; r.in_kind[j] = p->vars[v].kind;
+      } else {
+        r.in_row[j] = 0; r.in_sp[j] = -1; r.in_w[j] = 1; r.in_kind[j] = 0;
+      }
+    }
+    r.imm0 = o.imm0; r.imm1 = o.imm1; r.imm2 = o.imm2; r.bits = o.bits;
+    if (o.opcode == LS_OP_LEAPFROG) {  // side outputs as rows (g may be dead: -1)
+      const int gv = (int)(o.bits & 0xffffffff), iv = (int)(o.bits >> 32);
+      const long long grow = gv >= 0 ? row_of(gv) : -1;
+      r.bits = (long long)((unsigned long long)(grow & 0xffffffff) | ((unsigned long long)row_of(iv) << 32));
+    }
+    rops[i] = r;
+  }
+  rblocks.resize(p->blocks.size());
+  for (size_t b = 0; b < p->blocks.size(); ++b) {
+    const ls_block& o = p->blocks[b];
+    RBlock r{};
+    r.op_begin = o.op_begin; r.op_count = o.op_count; r.term = o.term; r.a = o.a; r.b = o.b;
+    r.grads = o.grads;
+    if (o.term == LS_BRANCH) {
+      r.cond_row = row_of(o.cond); r.cond_sp = sp_of(o.cond); r.cond_w = p->vars[o.cond].width;
+    } else {
+      r.cond_row = 0; r.cond_sp = -1; r.cond_w = 1;
+    }
+    rblocks[b] = r;
+  }
+}
+
+static VMArgs make_args(ls_machine* m, long long max_steps) {
+  ls_program* p = m->p;
+  VMArgs a{};
+  a.blocks = m->d_blocks; a.ops = m->d_ops;
+  a.n_blocks = (int)p->blocks.size(); a.halt = (int)p->blocks.size(); a.entry = p->entry;
+  a.n_inputs = (int)p->inputs.size(); a.input_rows = m->d_input_rows;
+  a.output_row = m->var_row[p->output];
+  a.output_sp = p->vars[p->output].cls == LS_STACKED ? p->vars[p->output].sp : -1;
+  a.out_width = m->out_width;
+  a.n_sp_rows = p->n_stacked + 1;
+  for (int i = 0; i < kMaxTargets; ++i) a.targets[i] = p->targets[i];
+  a.z = m->z; a.depth = m->depth; a.lanes = m->lanes; a.group_rows = m->group_rows;
+  a.ws = m->ws; a.sp = m->sp; a.pcs = m->pcs; a.chain_of = m->chain_of;
+  a.inputs = (const uint64_t* const*)m->d_input_ptrs; a.input_width = m->d_input_width;
+  a.output = m->output;
+  a.next_chain = m->counters + 0;
+  a.refill = m->refill;
+  a.sched = m->opts.sched;
+  a.exact_logpdf = m->opts.exact_logpdf;
+  a.max_steps = max_steps;
+  a.group_steps = m->group_steps; a.group_done = m->group_done;
+  a.trace_block = m->trace_block; a.trace_active = m->trace_active;
+  a.trace_cap = m->trace_cap; a.trace_n = m->trace_n;
+  a.blk_steps = m->blk_steps; a.blk_active = m->blk_active;
+  a.useful = m->counters + 1; a.launched = m->counters + 2;
+  a.n_groups = m->groups;
+  a.lf_smem_per_warp = m->lf_smem_per_warp;
+  a.lane_trace = m->lane_trace; a.lane_trace_len = m->lane_trace_len; a.lane_trace_cap = m->lane_trace_cap;
+  a.fault = m->fault; a.abort_flag = m->flags + 0; a.paused = m->flags + 1;
+  return a;
+}
+
+extern "C" {
+
+int ls_abi_version(void) { return LS_ABI_VERSION; }
+
+const char* ls_last_error(void) { return g_err.c_str(); }
+
+int ls_device_count(int32_t* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *n = 0;
+    cudaGetLastError();
+    return fail(LS_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *n = c;
+  return LS_OK;
+}
+
+int ls_program_create(const ls_program_desc* d, ls_program** out) {
+  if (!d || !out || d->n_blocks < 1 || d->n_vars < 1) return fail(LS_EINVAL, "empty program");
+  auto* p = new ls_program();
+  p->blocks.assign(d->blocks, d->blocks + d->n_blocks);
+  p->ops.assign(d->ops, d->ops + d->n_ops);
+  p->vars.assign(d->vars, d->vars + d->n_vars);
+  p->inputs.assign(d->inputs, d->inputs + d->n_inputs);
+  p->entry = d->entry;
+  p->output = d->output;
+  p->flat_rows = d->flat_rows;
+  for (auto& v : p->vars)
+    if (v.cls == LS_STACKED) p->n_stacked = std::max(p->n_stacked, v.sp + 1);
+  for (auto& b : p->blocks) {
+    if (b.op_begin < 0 || b.op_begin + b.op_count > d->n_ops) {
+      delete p;
+      return fail(LS_EINVAL, "block op range");
+    }
+  }
+  *out = p;
+  return LS_OK;
+}
+
+int ls_program_bind_target(ls_program* p, int32_t slot, int32_t kind, int32_t dim, int32_t n,
+                           const double* params, double norm) {
+  if (!p || slot < 0 || slot >= kMaxTargets || dim < 1) return fail(LS_EINVAL, "bad target slot");
+  const int rows = kind == LS_TARGET_GAUSSIAN ? dim : n;
+  if (rows < 1) return fail(LS_EINVAL, "bad target shape");
+  std::vector<double> h(params, params + (size_t)rows * dim), ht((size_t)rows * dim);
+  for (int i = 0; i < rows; ++i)
+    for (int j = 0; j < dim; ++j) ht[(size_t)j * rows + i] = h[(size_t)i * dim + j];
+  double *dP = nullptr, *dPT = nullptr;
+  int rc;
+  if ((rc = upload(&dP, h)) || (rc = upload(&dPT, ht))) return rc;
+  p->owned.push_back(dP);
+  p->owned.push_back(dPT);
+  DevTarget t{};
+  t.kind = kind; t.dim = dim; t.n = n; t.P = dP; t.PT = dPT; t.norm = norm;
+  // B operand(s) in DMMA fragment order: Bf[(ks*NT + nt)*32 + l] = B[4ks + l%4][8nt + l/4]
+  auto frag = [&](int K, int N, auto at, const double** dst, int* KS, int* NT) -> int {
+    *KS = (K + 3) / 4;
+    *NT = (N + 7) / 8;
+    std::vector<double> f((size_t)(*KS) * (*NT) * 32, 0.0);
+    for (int ks = 0; ks < *KS; ++ks)
+      for (int nt = 0; nt < *NT; ++nt)
+        for (int l = 0; l < 32; ++l) {
+          const int k = 4 * ks + l % 4, c = 8 * nt + l / 4;
+          if (k < K && c < N) f[((size_t)ks * (*NT) + nt) * 32 + l] = at(k, c);
+        }
+    double* df = nullptr;
+    int rc2 = upload(&df, f);
+    if (rc2) return rc2;
+    p->owned.push_back(df);
+    *dst = df;
+    return LS_OK;
+  };
+  if (kind == LS_TARGET_GAUSSIAN) {
+    if ((rc = frag(dim, dim, [&](int k, int c) { return h[(size_t)k * dim + c]; }, &t.B1, &t.KS1, &t.NT1))) return rc;
+  } else {
+    if ((rc = frag(dim, n, [&](int k, int c) { return h[(size_t)c * dim + k]; }, &t.B1, &t.KS1, &t.NT1))) return rc;
+    if ((rc = frag(n, dim, [&](int k, int c) { return h[(size_t)k * dim + c]; }, &t.B2, &t.KS2, &t.NT2))) return rc;
+  }
+  p->targets[slot] = t;
+  return LS_OK;
+}
+
+int ls_program_destroy(ls_program* p) {
+  if (!p) return LS_OK;
+  for (double* q : p->owned) cudaFree(q);
+  delete p;
+  return LS_OK;
+}
+
+int ls_machine_destroy(ls_machine* m) {
+  if (!m) return LS_OK;
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  cudaFree(m->d_blocks); cudaFree(m->d_ops); cudaFree(m->d_input_width); cudaFree(m->d_input_rows);
+  cudaFree(m->ws); cudaFree(m->sp); cudaFree(m->pcs); cudaFree(m->chain_of);
+  for (auto* q : m->inputs) cudaFree(q);
+  cudaFree(m->d_input_ptrs); cudaFree(m->output); cudaFree(m->counters);
+  cudaFree(m->group_steps); cudaFree(m->group_done); cudaFree(m->trace_block);
+  cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
+  cudaFree(m->blk_active); cudaFree(m->fault); cudaFree(m->flags);
+  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len);
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
+  if (m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+  return LS_OK;
+}
+
+static int reset_state(ls_machine* m) {
+  const size_t L = m->lanes, nb = m->p->blocks.size();
+  const int n_sp_rows = m->p->n_stacked + 1;
+  CK(cudaMemsetAsync(m->sp, 0, (size_t)m->groups * n_sp_rows * L * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->pcs, 0, (size_t)m->groups * (m->depth + 1) * L * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->counters, 0, 4 * sizeof(unsigned long long), m->stream));
+  CK(cudaMemsetAsync(m->group_steps, 0, m->groups * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->group_done, 0, m->groups * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->blk_steps, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->blk_active, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->flags, 0, 4 * sizeof(int), m->stream));
+  CK(cudaMemsetAsync(m->trace_n, 0, sizeof(long long), m->stream));
+  if (m->lane_trace_len) CK(cudaMemsetAsync(m->lane_trace_len, 0, (size_t)m->z * sizeof(int), m->stream));
+  FaultRec f0{~0ull, 0, 0, 0, 0, -1};
+  CK(cudaMemcpyAsync(m->fault, &f0, sizeof(f0), cudaMemcpyHostToDevice, m->stream));
+  std::vector<long long> slots((size_t)m->groups * L, -1);
+  if (!m->refill)
+    for (size_t t = 0; t < L; ++t) slots[t] = (long long)t < m->z ? (long long)t : -2;
+  CK(cudaMemcpyAsync(m->chain_of, slots.data(), slots.size() * sizeof(long long), cudaMemcpyHostToDevice,
+                     m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  m->started = false;
+  return static_init(m);
+}
+
+int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_opts* opts,
+                      ls_machine** out) {
+  if (!p || !out || z < 1 || depth < 1) return fail(LS_EINVAL, "bad machine arguments");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(LS_ECUDA, "no CUDA device: the lockstep B200 engine has no CPU fallback");
+  }
+  auto* m = new ls_machine();
+  m->p = p;
+  m->z = z;
+  m->depth = depth;
+  if (opts) m->opts = *opts;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int groups;
+  m->warp = m->opts.warp_groups != 0;
+  if (m->warp) {
+    // one 32-lane group per warp, 4 warps per CTA; default: a group per 32 chains,
+    // capped at 16 resident warps per SM
+    m->lanes = 32;
+    const long long want = (z + 31) / 32;
+    groups = m->opts.ctas > 0 ? 4 * m->opts.ctas : (int)std::min<long long>(want, (long long)sms * 16);
+    if (groups > want) groups = (int)want;
+    m->refill = true;
+    for (const auto& op : p->ops)
+      if (op.opcode == LS_OP_LEAPFROG)
+        m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, lf_smem_doubles(p->targets[op.imm0].dim));
+  } else {
+    int lanes = m->opts.lanes_per_cta > 0 ? m->opts.lanes_per_cta : (int)std::min<long long>(z, kMaxLanes);
+    if (m->opts.lanes_per_cta <= 0 && z > kMaxLanes) {
+      delete m;
+      return fail(LS_EINVAL, "a single schedule group holds at most 1024 lanes; set lanes_per_cta");
+    }
+    lanes = std::min(kMaxLanes, ((lanes + 31) / 32) * 32);
+    m->lanes = lanes;
+    m->refill = z > lanes;
+    const long long want = (z + lanes - 1) / lanes;
+    groups = m->opts.ctas > 0 ? m->opts.ctas : sms * std::max(1, 1024 / lanes);
+    if (!m->refill) groups = 1;
+    if (groups > want) groups = (int)want;
+  }
+  m->groups = groups;
+  if (m->opts.trace && groups != 1) {
+    delete m;
+    return fail(LS_EINVAL, "per-step traces need a single schedule group (z <= lanes_per_cta)");
+  }
+  // storage layout: the lowering placed every non-stacked variable in the flat
+  // region; stacked variables follow with depth slots each
+  const auto& vars = p->vars;
+  m->var_row.resize(vars.size());
+  m->var_depth.resize(vars.size());
+  int rows = p->flat_rows;
+  for (size_t v = 0; v < vars.size(); ++v) {
+    const int slots = vars[v].cls == LS_STACKED ? depth : 1;
+    m->var_depth[v] = slots;
+    if (vars[v].cls == LS_STACKED) {
+      m->var_row[v] = rows;
+      rows += slots * vars[v].width;
+    } else {
+      m->var_row[v] = vars[v].row;
+      if (vars[v].row < 0 || vars[v].row + vars[v].width > p->flat_rows) {
+        delete m;
+        return fail(LS_EINVAL, "variable rows outside the flat region");
+      }
+    }
+  }
+  m->group_rows = rows;
+  m->out_width = vars[p->output].width;
+  for (int v : p->inputs) {
+    m->input_width.push_back(vars[v].width);
+    m->input_rows.push_back(m->var_row[v]);
+  }
+  const int n_sp_rows = p->n_stacked + 1;
+  const size_t L = m->lanes;
+  std::vector<ROp> rops;
+  std::vector<RBlock> rblocks;
+  resolve(m, rops, rblocks);
+  int rc = 0;
+  CK(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  if ((rc = upload(&m->d_ops, rops)) || (rc = upload(&m->d_blocks, rblocks)) ||
+      (rc = upload(&m->d_input_width, m->input_width)) || (rc = upload(&m->d_input_rows, m->input_rows)) ||
+      (rc = dalloc(&m->ws, (size_t)groups * rows * L)) ||
+      (rc = dalloc(&m->sp, (size_t)groups * n_sp_rows * L)) ||
+      (rc = dalloc(&m->pcs, (size_t)groups * (depth + 1) * L)) ||
+      (rc = dalloc(&m->chain_of, (size_t)groups * L)) ||
+      (rc = dalloc(&m->d_input_ptrs, std::max<size_t>(1, p->inputs.size()))) ||
+      (rc = dalloc(&m->output, (size_t)z * m->out_width)) ||
+      (rc = dalloc(&m->counters, 4)) || (rc = dalloc(&m->group_steps, groups)) ||
+      (rc = dalloc(&m->group_done, groups)) ||
+      (rc = dalloc(&m->blk_steps, (size_t)groups * p->blocks.size())) ||
+      (rc = dalloc(&m->blk_active, (size_t)groups * p->blocks.size())) ||
+      (rc = dalloc(&m->fault, 1)) || (rc = dalloc(&m->flags, 4)) || (rc = dalloc(&m->trace_n, 1))) {
+    ls_machine_destroy(m);
+    return rc;
+  }
+  for (size_t k = 0; k < p->inputs.size(); ++k) {
+    uint64_t* buf = nullptr;
+    if ((rc = dalloc(&buf, (size_t)z * m->input_width[k]))) {
+      ls_machine_destroy(m);
+      return rc;
+    }
+    cudaMemsetAsync(buf, 0, (size_t)z * m->input_width[k] * 8, m->stream);
+    m->inputs.push_back(buf);
+  }
+  if (!m->inputs.empty())
+    CK(cudaMemcpy(m->d_input_ptrs, m->inputs.data(), m->inputs.size() * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+  // the reference zero-fills all storage at init (pc_vm.py:171-181)
+  CK(cudaMemsetAsync(m->ws, 0, (size_t)groups * rows * L * sizeof(uint64_t), m->stream));
+  CK(cudaMemsetAsync(m->output, 0, (size_t)z * m->out_width * sizeof(uint64_t), m->stream));
+  if (m->opts.lane_trace_cap > 0) {
+    m->lane_trace_cap = m->opts.lane_trace_cap;
+    if ((rc = dalloc(&m->lane_trace, (size_t)z * m->lane_trace_cap)) || (rc = dalloc(&m->lane_trace_len, (size_t)z))) {
+      ls_machine_destroy(m);
+      return rc;
+    }
+  }
+  if (m->opts.trace) {
+    m->trace_cap = 1 << 16;
+    if ((rc = dalloc(&m->trace_block, m->trace_cap)) || (rc = dalloc(&m->trace_active, m->trace_cap))) {
+      ls_machine_destroy(m);
+      return rc;
+    }
+  }
+  if ((rc = reset_state(m))) {
+    ls_machine_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return LS_OK;
+}
+
+int ls_machine_reset(ls_machine* m) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  return reset_state(m);
+}
+
+int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes) {
+  if (!m || idx < 0 || idx >= (int)m->inputs.size()) return fail(LS_EINVAL, "bad input index");
+  if (bytes != m->z * m->input_width[idx] * 8) return fail(LS_EINVAL, "input size mismatch");
+  CK(cudaMemcpyAsync(m->inputs[idx], host, bytes, cudaMemcpyHostToDevice, m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  return static_init(m);
+}
+
+int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes) {
+  if (!m || idx < 0 || idx >= (int)m->inputs.size()) return fail(LS_EINVAL, "bad input index");
+  if (bytes != m->z * m->input_width[idx] * 8) return fail(LS_EINVAL, "input size mismatch");
+  CK(cudaMemcpyAsync(m->inputs[idx], dev, bytes, cudaMemcpyDeviceToDevice, m->stream));
+  return static_init(m);
+}
+
+}  // extern "C"
+
+// Single-group machines are seeded eagerly (pc stack [halt, entry], one live
+// slot per data stack, inputs in slot 0) so observers can inspect them before
+// the first step; refilling machines seed each lane when it takes a chain.
+static int static_init(ls_machine* m) {
+  if (m->refill || m->started) return LS_OK;
+  VMArgs a = make_args(m, 0);
+  init_static_kernel<<<1, m->lanes, 0, m->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
+extern "C" {
+
+int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
+  if (!m || !st) return fail(LS_EINVAL, "null machine");
+  ls_program* p = m->p;
+  VMArgs a = make_args(m, max_steps);
+  m->started = true;
+  size_t smem = m->warp ? (size_t)4 * m->lf_smem_per_warp * sizeof(double)
+                        : (p->blocks.size() + 1) * sizeof(int);
+  if (smem > 48 * 1024) {
+    if (m->warp) CK(cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    else CK(cudaFuncSetAttribute(vm_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  CK(cudaMemsetAsync(m->flags + 1, 0, 2 * sizeof(int), m->stream));
+  if (!m->ev0) {
+    CK(cudaEventCreate(&m->ev0));
+    CK(cudaEventCreate(&m->ev1));
+  }
+  CK(cudaEventRecord(m->ev0, m->stream));
+  if (m->warp) vm_warp_kernel<<<(m->groups + 3) / 4, 128, smem, m->stream>>>(a);
+  else vm_cta_kernel<<<m->groups, m->lanes, smem, m->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(m->ev1, m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+  m->launches += 1;
+  int flags[3];
+  FaultRec f;
+  std::vector<long long> gsteps(m->groups);
+  std::vector<int> gdone(m->groups);
+  unsigned long long cnt[3];
+  CK(cudaMemcpy(flags, m->flags, sizeof(flags), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&f, m->fault, sizeof(f), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(gsteps.data(), m->group_steps, m->groups * sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(gdone.data(), m->group_done, m->groups * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt, m->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
+  std::memset(st, 0, sizeof(*st));
+  st->steps = *std::max_element(gsteps.begin(), gsteps.end());
+  st->useful_grads = (int64_t)cnt[1];
+  st->launched_grads = (int64_t)cnt[2];
+  st->kernel_ms = ms;
+  st->launches = m->launches;
+  st->var = -1;
+  if (flags[0]) {
+    st->kind = f.kind;
+    st->var = f.var;
+    st->lane = f.chain;
+    st->block = f.block;
+    st->pad = f.detail;
+    return LS_OK;
+  }
+  bool all_done = true;
+  for (int d : gdone) all_done = all_done && d;
+  if (all_done) st->kind = LS_RUN_HALTED;
+  else if (flags[1] && max_steps >= 0 && st->steps >= max_steps) st->kind = LS_RUN_STEP_LIMIT;
+  else st->kind = LS_RUN_PAUSED;
+  return LS_OK;
+}
+
+int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
+  CK(cudaMemcpyAsync(host, m->output, bytes, cudaMemcpyDeviceToHost, m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
+int ls_output_device(ls_machine* m, void** dev) {
+  if (!m || !dev) return fail(LS_EINVAL, "null machine");
+  *dev = m->output;
+  return LS_OK;
+}
+
+int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap, int64_t* n) {
+  if (!m || !n) return fail(LS_EINVAL, "null machine");
+  *n = 0;
+  if (!m->trace_block) return LS_OK;
+  long long have = 0;
+  CK(cudaMemcpy(&have, m->trace_n, sizeof(have), cudaMemcpyDeviceToHost));
+  const long long k = std::min<long long>(have, cap);
+  if (k > 0) {
+    CK(cudaMemcpy(blocks, m->trace_block, k * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(active, m->trace_active, k * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  if (k < have) {  // keep the undrained tail at the front
+    std::vector<int> rb(have - k), ra(have - k);
+    CK(cudaMemcpy(rb.data(), m->trace_block + k, (have - k) * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ra.data(), m->trace_active + k, (have - k) * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(m->trace_block, rb.data(), rb.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(m->trace_active, ra.data(), ra.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  const long long rest = have - k;
+  CK(cudaMemcpy(m->trace_n, &rest, sizeof(rest), cudaMemcpyHostToDevice));
+  *n = k;
+  return LS_OK;
+}
+
+int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  const size_t nb = m->p->blocks.size();
+  std::vector<long long> s((size_t)m->groups * nb), a((size_t)m->groups * nb);
+  CK(cudaMemcpy(s.data(), m->blk_steps, s.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(a.data(), m->blk_active, a.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  for (size_t b = 0; b < nb; ++b) {
+    long long ss = 0, aa = 0;
+    for (int g = 0; g < m->groups; ++g) {
+      ss += s[(size_t)g * nb + b];
+      aa += a[(size_t)g * nb + b];
+    }
+    steps[b] = ss;
+    active[b] = aa;
+  }
+  return LS_OK;
+}
+
+int ls_read_var(ls_machine* m, int32_t var, void* host, int64_t bytes) {
+  if (!m || var < 0 || var >= (int)m->p->vars.size()) return fail(LS_EINVAL, "bad var");
+  if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
+  const int slots = m->var_depth[var], w = m->p->vars[var].width;
+  const long long z = m->z;
+  if (bytes != (int64_t)slots * z * w * 8) return fail(LS_EINVAL, "var size mismatch");
+  std::vector<uint64_t> raw((size_t)slots * w * m->lanes);
+  CK(cudaMemcpy(raw.data(), m->ws + (size_t)m->var_row[var] * m->lanes, raw.size() * 8, cudaMemcpyDeviceToHost));
+  auto* dst = static_cast<uint64_t*>(host);
+  for (int s = 0; s < slots; ++s)
+    for (long long l = 0; l < z; ++l)
+      for (int i = 0; i < w; ++i) dst[((size_t)s * z + l) * w + i] = raw[((size_t)s * w + i) * m->lanes + l];
+  return LS_OK;
+}
+
+int ls_read_pointers(ls_machine* m, int32_t var, int64_t* host, int64_t z) {
+  if (!m || z != m->z) return fail(LS_EINVAL, "bad pointer request");
+  if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
+  int row;
+  if (var < 0) row = m->p->n_stacked;
+  else if (m->p->vars[var].cls == LS_STACKED) row = m->p->vars[var].sp;
+  else return fail(LS_EINVAL, "not a stacked variable");
+  std::vector<int> raw(m->lanes);
+  CK(cudaMemcpy(raw.data(), m->sp + (size_t)row * m->lanes, m->lanes * sizeof(int), cudaMemcpyDeviceToHost));
+  for (long long l = 0; l < z; ++l) host[l] = raw[l];
+  return LS_OK;
+}
+
+int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count) {
+  if (!m || count != (int64_t)(m->depth + 1) * m->z) return fail(LS_EINVAL, "bad pc request");
+  if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
+  std::vector<int> raw((size_t)(m->depth + 1) * m->lanes);
+  CK(cudaMemcpy(raw.data(), m->pcs, raw.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int s = 0; s <= m->depth; ++s)
+    for (long long l = 0; l < m->z; ++l) host[(size_t)s * m->z + l] = raw[(size_t)s * m->lanes + l];
+  return LS_OK;
+}
+
+int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap) {
+  if (!m || !m->lane_trace) return fail(LS_EINVAL, "machine was created without lane traces");
+  if (cap != m->lane_trace_cap) return fail(LS_EINVAL, "lane trace capacity mismatch");
+  CK(cudaMemcpy(blocks, m->lane_trace, (size_t)m->z * cap * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(lens, m->lane_trace_len, (size_t)m->z * sizeof(int), cudaMemcpyDeviceToHost));
+  return LS_OK;
+}
+
+int ls_machine_sync(ls_machine* m) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
+int ls_rng_uniform(const int64_t* key, const int64_t* counter, int64_t n, double* out) {
+  if (n <= 0) return LS_OK;
+  int64_t *dk = nullptr, *dc = nullptr;
+  double* dout = nullptr;
+  int rc;
+  if ((rc = dalloc(&dk, n)) || (rc = dalloc(&dc, n)) || (rc = dalloc(&dout, n))) {
+    cudaFree(dk);
+    cudaFree(dc);
+    return rc;
+  }
+  cudaMemcpy(dk, key, n * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dc, counter, n * 8, cudaMemcpyHostToDevice);
+  rng_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dk, dc, n, dout);
+  cudaError_t e = cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost);
+  cudaFree(dk);
+  cudaFree(dc);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(LS_ECUDA, cudaGetErrorString(e));
+  return LS_OK;
+}
+
+int ls_target_eval(int32_t kind, int32_t which, int32_t dim, int32_t n, const double* params, double norm,
+                   const double* x, int64_t z, double* out) {
+  if (z <= 0) return LS_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(LS_ECUDA, "no CUDA device: the lockstep B200 engine has no CPU fallback");
+  }
+  ls_program tmp;
+  int rc = ls_program_bind_target(&tmp, 0, kind, dim, n, params, norm);
+  if (rc) {
+    for (double* q : tmp.owned) cudaFree(q);
+    return rc;
+  }
+  double *dx = nullptr, *dout = nullptr;
+  uint64_t* scratch = nullptr;
+  const size_t outn = which == 0 ? (size_t)z : (size_t)z * dim;
+  if ((rc = dalloc(&dx, (size_t)z * dim)) || (rc = dalloc(&dout, outn)) ||
+      (rc = dalloc(&scratch, (size_t)2 * z * dim))) {
+    cudaFree(dx);
+    cudaFree(dout);
+    for (double* q : tmp.owned) cudaFree(q);
+    return rc;
+  }
+  cudaMemcpy(dx, x, (size_t)z * dim * 8, cudaMemcpyHostToDevice);
+  target_eval_kernel<<<(unsigned)((z + 127) / 128), 128>>>(tmp.targets[0], which, dx, z, dout, scratch);
+  cudaError_t e = cudaMemcpy(out, dout, outn * 8, cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dout);
+  cudaFree(scratch);
+  for (double* q : tmp.owned) cudaFree(q);
+  if (e != cudaSuccess) return fail(LS_ECUDA, cudaGetErrorString(e));
+  return LS_OK;
+}
+
+}  // extern "C"

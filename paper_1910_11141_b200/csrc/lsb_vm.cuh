@@ -1,0 +1,621 @@
+// lsb_vm.cuh — device core of the B200 program-counter VM: machine layout,
+// op execution, warp-cooperative target contractions, fused superblocks.
+//
+// Storage. Every group of L lanes owns a workspace of `group_rows` rows of L
+// 8-byte words ("lane-minor": element i of a lane's vector lives at row
+// base+i, column = lane), so one warp touching element i of 32 lanes issues a
+// single coalesced 256-byte access. Non-stacked variables have fixed rows
+// laid out by the lowering (temporaries share an arena; views alias rows);
+// stacked variables own depth x width rows and a per-lane stack pointer, the
+// top slot being the one under the pointer (reference runtime.py:442-512).
+//
+// Ops arrive "resolved" (ROp): the machine precomputes each operand's base
+// row, stack-pointer row and width, so executing an op costs one descriptor
+// read plus the data accesses — no per-operand table walks.
+#pragma once
+#include <cstdint>
+
+#include "../../include/lockstep_b200.h"
+#include "lsb_dmma.cuh"
+#include "lsb_ops.cuh"
+
+namespace lsbvm {
+
+using lsb::as_f64;
+using lsb::f64_bits;
+
+constexpr int kMaxTargets = 8;
+constexpr int kMaxLanes = 1024;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct DevTarget {
+  int kind = 0, dim = 0, n = 0;
+  const double* P = nullptr;   // gaussian: precision (d x d, row-major); logreg: sx (n x d)
+  const double* PT = nullptr;  // transpose of the above
+  double norm = 0.0;
+  // DMMA B operands in fragment order (lsb_dmma.cuh)
+  const double* B1 = nullptr;  // gaussian: P (d x d);   logreg: sx^T (d x n)
+  int KS1 = 0, NT1 = 0;
+  const double* B2 = nullptr;  // logreg: sx (n x d)
+  int KS2 = 0, NT2 = 0;
+};
+
+// One op with its operands resolved against the machine's storage layout.
+struct ROp {
+  int opcode, action, nin, kind;
+  int width;               // output width (words)
+  int out;                 // output (or popped) variable id, for fault reports
+  int out_row, out_sp;     // output base row; stack-pointer row or -1
+  int in_row[3], in_sp[3], in_w[3], in_kind[3];
+  int imm0, imm1, imm2, pad;
+  long long bits;          // const payload; superblock: g_row | i_row << 32 (rows, -1 = none)
+};
+
+struct RBlock {
+  int op_begin, op_count, term, a, b, grads;
+  int cond_row, cond_sp, cond_w;
+  int pad;
+};
+
+struct FaultRec {
+  unsigned long long key;  // lowest wins
+  int kind;                // LS_RUN_OVERFLOW / LS_RUN_UNDERFLOW
+  int var;                 // -1 = pc stack
+  int block;
+  int detail;              // 1 = underflow of an update (write_top)
+  long long chain;
+};
+
+struct VMArgs {
+  const RBlock* blocks;
+  const ROp* ops;
+  int n_blocks, halt, entry;
+  int n_inputs;
+  const int* input_rows;        // slot-0 base row of each input var
+  int output_row, output_sp, out_width;
+  int n_sp_rows;                // stacked vars + 1 (pc)
+  DevTarget targets[kMaxTargets];
+  long long z;
+  int depth;
+  int lanes;                    // lanes per group
+  int group_rows;
+  uint64_t* ws;
+  int* sp;                      // [groups][n_sp_rows][lanes]
+  int* pcs;                     // [groups][depth+1][lanes]
+  long long* chain_of;          // [groups][lanes]  (-1 free, -2 exhausted)
+  const uint64_t* const* inputs;
+  const int* input_width;
+  uint64_t* output;             // [z][out_width]
+  unsigned long long* next_chain;
+  int refill, sched, exact_logpdf;
+  long long max_steps;
+  long long* group_steps;
+  int* group_done;
+  int* trace_block;
+  int* trace_active;
+  long long trace_cap;
+  long long* trace_n;
+  long long* blk_steps;
+  long long* blk_active;
+  unsigned long long* useful;
+  unsigned long long* launched;
+  int n_groups;
+  int lf_smem_per_warp;
+  int* lane_trace;
+  int* lane_trace_len;
+  int lane_trace_cap;
+  FaultRec* fault;
+  int* abort_flag;
+  int* paused;
+};
+
+struct Lane {
+  uint64_t* ws;  // group workspace
+  int* sp;       // group stack pointers
+  int* pcs;      // group pc stack
+  int t, L;
+
+  __device__ __forceinline__ uint64_t* row(int r) const { return ws + (size_t)r * L + t; }
+  __device__ __forceinline__ int& sp_row(int s) const { return sp[s * L + t]; }
+  // current top of a variable given its base row / sp row / width
+  __device__ __forceinline__ uint64_t* top(int base, int s, int w) const {
+    if (s >= 0) {
+      int p = sp_row(s) - 1;
+      base += (p < 0 ? 0 : p) * w;
+    }
+    return row(base);
+  }
+  __device__ __forceinline__ const uint64_t* in(const ROp& op, int j) const {
+    return top(op.in_row[j], op.in_sp[j], op.in_w[j]);
+  }
+};
+
+__device__ __forceinline__ int64_t as_i64_any(uint64_t w, int kind) {
+  return kind == LS_F64 ? lsb::f64_to_i64(as_f64(w)) : (int64_t)w;
+}
+
+// ---- per-lane target densities (reference workloads.py:186-228) --------------------
+
+struct LrMargin {  // p(i) = logaddexp(0, -m_i) with m_i = w . sx_i
+  const uint64_t* w;
+  int stride, d;
+  const double* sx;
+  __device__ double operator()(int i) const {
+    const double* r = sx + (size_t)i * d;
+    double m = 0.0;
+    for (int j = 0; j < d; ++j) m = fma(as_f64(w[(size_t)j * stride]), __ldg(r + j), m);
+    return lsb::np_logaddexp(0.0, -m);
+  }
+};
+
+__device__ inline double target_logpdf(const DevTarget& tg, const uint64_t* x, int stride, int exact) {
+  if (tg.kind == LS_TARGET_GAUSSIAN) {
+    if (exact) return lsb::gauss_logpdf_exact(x, stride, tg.dim, tg.P, tg.norm);
+    double acc = 0.0;
+    for (int j = 0; j < tg.dim; ++j) {
+      const double* col = tg.PT + (size_t)j * tg.dim;
+      double px = 0.0;
+      for (int i = 0; i < tg.dim; ++i) px = fma(as_f64(x[(size_t)i * stride]), __ldg(col + i), px);
+      acc = fma(as_f64(x[(size_t)j * stride]), px, acc);
+    }
+    return tg.norm - 0.5 * acc;
+  }
+  const double lik = lsb::pairwise(LrMargin{x, stride, tg.dim, tg.P}, 0, tg.n);
+  const double ww = lsb::dot_lane(x, x, tg.dim, stride);
+  return __dsub_rn(-__dadd_rn(0.0, lik), __dmul_rn(0.5, ww));
+}
+
+__device__ inline void target_grad(const DevTarget& tg, const uint64_t* x, int stride, uint64_t* out) {
+  const int d = tg.dim;
+  if (tg.kind == LS_TARGET_GAUSSIAN) {
+    for (int j = 0; j < d; ++j) {
+      const double* col = tg.PT + (size_t)j * d;
+      double acc = 0.0;
+      for (int i = 0; i < d; ++i) acc = fma(as_f64(x[(size_t)i * stride]), __ldg(col + i), acc);
+      out[(size_t)j * stride] = f64_bits(-acc);
+    }
+    return;
+  }
+  for (int j = 0; j < d; ++j) out[(size_t)j * stride] = f64_bits(0.0);
+  for (int i = 0; i < tg.n; ++i) {
+    const double* r = tg.P + (size_t)i * d;
+    double m = 0.0;
+    for (int j = 0; j < d; ++j) m = fma(as_f64(x[(size_t)j * stride]), __ldg(r + j), m);
+    const double s = lsb::lr_sig(m);
+    for (int j = 0; j < d; ++j) {
+      uint64_t* o = out + (size_t)j * stride;
+      *o = f64_bits(fma(s, __ldg(r + j), as_f64(*o)));
+    }
+  }
+  for (int j = 0; j < d; ++j) {
+    uint64_t* o = out + (size_t)j * stride;
+    *o = f64_bits(__dsub_rn(as_f64(*o), as_f64(x[(size_t)j * stride])));
+  }
+}
+
+// Elementwise loop with 8 loads in flight before the stores (memory-level
+// parallelism for the latency-bound copies that dominate NUTS-lite's packing).
+// Loads-then-stores is safe when dst aliases an input element-for-element.
+template <class F>
+__device__ __forceinline__ void ew8(int w, uint64_t* dst, int L, const F& f) {
+  int i = 0;
+  for (; i + 8 <= w; i += 8) {
+    uint64_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = f(i + j);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[(size_t)(i + j) * L] = v[j];
+  }
+  for (; i < w; ++i) dst[(size_t)i * L] = f(i);
+}
+
+// Computes op into dst for one lane. x, y, u: current tops of the inputs.
+__device__ inline void compute_op(const VMArgs& a, const ROp& op, const uint64_t* x, const uint64_t* y,
+                                  const uint64_t* u, uint64_t* dst, int L) {
+  const int w = op.width;
+  const bool f = op.kind == LS_F64;
+#define X(i) x[(size_t)(i) * L]
+#define Y(i) y[(size_t)(i) * L]
+#define U(i) u[(size_t)(i) * L]
+#define D(i) dst[(size_t)(i) * L]
+  switch (op.opcode) {
+    case LS_OP_CONST: D(0) = (uint64_t)op.bits; break;
+    case LS_OP_ID: if (dst != x) ew8(w, dst, L, [&](int i) { return X(i); }); break;
+    case LS_OP_ADD:
+      if (f) ew8(w, dst, L, [&](int i) { return f64_bits(__dadd_rn(as_f64(X(i)), as_f64(Y(i)))); });
+      else ew8(w, dst, L, [&](int i) { return X(i) + Y(i); });
+      break;
+    case LS_OP_SUB:
+      if (f) ew8(w, dst, L, [&](int i) { return f64_bits(__dsub_rn(as_f64(X(i)), as_f64(Y(i)))); });
+      else ew8(w, dst, L, [&](int i) { return X(i) - Y(i); });
+      break;
+    case LS_OP_MUL:
+      if (f) ew8(w, dst, L, [&](int i) { return f64_bits(__dmul_rn(as_f64(X(i)), as_f64(Y(i)))); });
+      else ew8(w, dst, L, [&](int i) { return (uint64_t)((unsigned long long)X(i) * (unsigned long long)Y(i)); });
+      break;
+    case LS_OP_DIV:
+      ew8(w, dst, L, [&](int i) -> uint64_t {
+        if (f) return f64_bits(__ddiv_rn(as_f64(X(i)), as_f64(Y(i))));
+        const int64_t p = (int64_t)X(i), q = (int64_t)Y(i);  // numpy floor_divide, /0 -> 0
+        if (q == 0) return 0;
+        if (q == -1) return 0ull - (uint64_t)p;
+        int64_t r = p / q;
+        if ((p % q != 0) && ((p < 0) != (q < 0))) r -= 1;
+        return (uint64_t)r;
+      });
+      break;
+    case LS_OP_MIN:
+    case LS_OP_MAX: {
+      const bool mn = op.opcode == LS_OP_MIN;
+      ew8(w, dst, L, [&](int i) -> uint64_t {
+        if (f) {
+          const double p = as_f64(X(i)), q = as_f64(Y(i));
+          if (p != p) return f64_bits(p);
+          if (q != q) return f64_bits(q);
+          return f64_bits(mn ? (p <= q ? p : q) : (p >= q ? p : q));
+        }
+        const int64_t p = (int64_t)X(i), q = (int64_t)Y(i);
+        return (uint64_t)(mn ? (p < q ? p : q) : (p > q ? p : q));
+      });
+      break;
+    }
+    case LS_OP_LE: D(0) = f ? (as_f64(X(0)) <= as_f64(Y(0))) : ((int64_t)X(0) <= (int64_t)Y(0)); break;
+    case LS_OP_LT: D(0) = f ? (as_f64(X(0)) < as_f64(Y(0))) : ((int64_t)X(0) < (int64_t)Y(0)); break;
+    case LS_OP_EQ: D(0) = f ? (as_f64(X(0)) == as_f64(Y(0))) : (X(0) == Y(0)); break;
+    case LS_OP_AND: D(0) = (X(0) != 0) && (Y(0) != 0); break;
+    case LS_OP_OR: D(0) = (X(0) != 0) || (Y(0) != 0); break;
+    case LS_OP_NOT: D(0) = X(0) == 0; break;
+    case LS_OP_NEG:
+      ew8(w, dst, L, [&](int i) { return f ? f64_bits(-as_f64(X(i))) : (uint64_t)(0ull - X(i)); });
+      break;
+    case LS_OP_ABS:
+      ew8(w, dst, L, [&](int i) -> uint64_t {
+        if (f) return f64_bits(fabs(as_f64(X(i))));
+        const int64_t p = (int64_t)X(i);
+        return p < 0 ? (uint64_t)(0ull - (uint64_t)p) : (uint64_t)p;
+      });
+      break;
+    case LS_OP_SQRT: ew8(w, dst, L, [&](int i) { return f64_bits(__dsqrt_rn(as_f64(X(i)))); }); break;
+    case LS_OP_EXP: ew8(w, dst, L, [&](int i) { return f64_bits(exp(as_f64(X(i)))); }); break;
+    case LS_OP_LOG: ew8(w, dst, L, [&](int i) { return f64_bits(log(as_f64(X(i)))); }); break;
+    case LS_OP_SIN: ew8(w, dst, L, [&](int i) { return f64_bits(sin(as_f64(X(i)))); }); break;
+    case LS_OP_COS: ew8(w, dst, L, [&](int i) { return f64_bits(cos(as_f64(X(i)))); }); break;
+    case LS_OP_FLOOR: ew8(w, dst, L, [&](int i) { return f64_bits(floor(as_f64(X(i)))); }); break;
+    case LS_OP_SELECT: {
+      const uint64_t* src = X(0) != 0 ? y : u;
+      if (src != dst) ew8(w, dst, L, [&](int i) { return src[(size_t)i * L]; });
+      break;
+    }
+    case LS_OP_DOT: D(0) = f64_bits(lsb::dot_lane(x, y, op.in_w[0], L)); break;
+    case LS_OP_AXPY: {
+      const double s = as_f64(X(0));
+      ew8(w, dst, L, [&](int i) { return f64_bits(__dadd_rn(__dmul_rn(s, as_f64(Y(i))), as_f64(U(i)))); });
+      break;
+    }
+    case LS_OP_VGET: {
+      const int vw = op.in_w[0];
+      int64_t k = as_i64_any(Y(0), op.in_kind[1]);
+      k = k < 0 ? 0 : (k > vw - 1 ? vw - 1 : k);
+      D(0) = X(k);
+      break;
+    }
+    case LS_OP_VSTORE: {
+      int64_t k = as_i64_any(Y(0), op.in_kind[1]);
+      k = k < 0 ? 0 : (k > w - 1 ? w - 1 : k);
+      const uint64_t val = U(0);
+      if (dst != x) ew8(w, dst, L, [&](int i) { return X(i); });
+      D(k) = val;
+      break;
+    }
+    case LS_OP_VCAT: {
+      const int wa = op.in_w[0];
+      if (dst != x) ew8(wa, dst, L, [&](int i) { return X(i); });
+      ew8(w - wa, dst + (size_t)wa * L, L, [&](int i) { return Y(i); });
+      break;
+    }
+    case LS_OP_VFILL: {
+      const uint64_t v = X(0);
+      ew8(w, dst, L, [&](int) { return v; });
+      break;
+    }
+    case LS_OP_VSLICE:
+      if (dst != x + (size_t)op.imm0 * L) ew8(w, dst, L, [&](int i) { return X(op.imm0 + i); });
+      break;
+    case LS_OP_RNG: {
+      const int64_t k = as_i64_any(X(0), op.in_kind[0]);
+      const int64_t c = as_i64_any(Y(0), op.in_kind[1]);
+      D(0) = f64_bits(lsb::rng_uniform(k, c));
+      break;
+    }
+    case LS_OP_LOGPDF: D(0) = f64_bits(target_logpdf(a.targets[op.imm0], x, L, a.exact_logpdf)); break;
+    case LS_OP_GRAD: target_grad(a.targets[op.imm0], x, L, dst); break;
+    default: break;
+  }
+#undef X
+#undef Y
+#undef U
+#undef D
+}
+
+__device__ inline void write_output(const VMArgs& a, const Lane& ln, long long chain) {
+  const uint64_t* src = ln.top(a.output_row, a.output_sp, a.out_width);
+  uint64_t* dst = a.output + (size_t)chain * a.out_width;
+  for (int i = 0; i < a.out_width; ++i) dst[i] = src[(size_t)i * ln.L];
+}
+
+__device__ inline void init_lane(const VMArgs& a, const Lane& ln, long long chain) {
+  // data stacks hold one live slot from the start (reference pc_vm.py:180-181)
+  for (int r = 0; r + 1 < a.n_sp_rows; ++r) ln.sp_row(r) = 1;
+  for (int k = 0; k < a.n_inputs; ++k) {
+    const int w = a.input_width[k];
+    const uint64_t* src = a.inputs[k] + (size_t)chain * w;
+    uint64_t* dst = ln.row(a.input_rows[k]);
+    for (int i = 0; i < w; ++i) dst[(size_t)i * ln.L] = src[i];
+  }
+  // pc stack seeded [halt, entry], pointer 2 (reference pc_vm.py:199-203)
+  ln.pcs[0 * ln.L + ln.t] = a.halt;
+  ln.pcs[1 * ln.L + ln.t] = a.entry;
+  ln.sp_row(a.n_sp_rows - 1) = 2;
+}
+
+__device__ __forceinline__ void lane_trace_put(const VMArgs& a, long long chain, int block) {
+  const int n = a.lane_trace_len[chain];
+  if (n < a.lane_trace_cap) a.lane_trace[(size_t)chain * a.lane_trace_cap + n] = block;
+  a.lane_trace_len[chain] = n + 1;
+}
+
+// ---- warp-cooperative contractions (DMMA) ------------------------------------------------
+
+// row g (0..7) of m-tile mt: the (8*mt+g)-th participating lane, or -1
+__device__ __forceinline__ int mtile_lane(unsigned mask, int n, int mt, int g) {
+  const int idx = 8 * mt + g;
+  return idx < n ? (int)__fns(mask, 0, idx + 1) : -1;
+}
+
+// grad, or fast logpdf, of a gaussian target for every participating lane of the
+// warp (lane-minor storage, stride 32). xp/dst: this lane's input and output.
+__device__ inline void warp_gauss(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+                                  bool want_logpdf) {
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = __ballot_sync(kFull, part);
+  const int n = __popc(mask);
+  const int d = tg.dim;
+  for (int mt = 0; mt * 8 < n; ++mt) {
+    const int src = mtile_lane(mask, n, mt, lane >> 2);
+    const uint64_t* xg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)xp, src < 0 ? 0 : src);
+    uint64_t* dg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)dst, src < 0 ? 0 : src);
+    auto a_at = [&](int k) -> double { return (src >= 0 && k < d) ? as_f64(xg[(size_t)k * 32]) : 0.0; };
+    double quad = 0.0;
+    for (int nt0 = 0; nt0 < tg.NT1; nt0 += LSB_NT_CHUNK) {
+      const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
+      LSB_NT_DISPATCH(ntc, {
+        double acc[NTC][2];
+        lsb::mtile_gemm<NTC>(acc, tg.B1, tg.KS1, tg.NT1, nt0, a_at);
+        _Pragma("unroll")
+        for (int j = 0; j < NTC; ++j) {
+          _Pragma("unroll")
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * (nt0 + j) + 2 * (lane & 3) + e;
+            if (src >= 0 && col < d) {
+              if (want_logpdf) quad = fma(as_f64(xg[(size_t)col * 32]), acc[j][e], quad);
+              else dg[(size_t)col * 32] = f64_bits(-acc[j][e]);
+            }
+          }
+        }
+      });
+    }
+    if (want_logpdf) {
+      quad += __shfl_xor_sync(kFull, quad, 1);
+      quad += __shfl_xor_sync(kFull, quad, 2);
+      if (src >= 0 && (lane & 3) == 0) dg[0] = f64_bits(tg.norm - 0.5 * quad);
+    }
+  }
+}
+
+__device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
+  if (op.opcode == LS_OP_GRAD) return a.targets[op.imm0].kind == LS_TARGET_GAUSSIAN;
+  if (op.opcode == LS_OP_LOGPDF) return !a.exact_logpdf && a.targets[op.imm0].kind == LS_TARGET_GAUSSIAN;
+  return false;
+}
+
+// Shared-memory row strides (doubles) of the superblock tiles: DMMA A-fragment
+// loads (8 rows x 4 cols, 64-bit) and C-fragment epilogues (8 rows x 2 cols,
+// 128-bit) are bank-conflict free.
+__host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8 * 8; return s + ((12 - s % 16) + 16) % 16; }
+__host__ __device__ __forceinline__ int lf_stride_p(int d) { int s = (d + 7) / 8 * 8; return s + ((8 - s % 16) + 16) % 16; }
+__host__ __device__ __forceinline__ int lf_smem_doubles(int d) { return 8 * (lf_stride_q(d) + lf_stride_p(d)) + 8; }
+
+// Fused leapfrog superblock: the whole `leapfrog(q, p, e)` function of the
+// NUTS-lite program (reference workloads.py:461-472; flat blocks
+// leapfrog.b0..b3) for every participating lane, run to return, with q and p
+// resident in shared memory across all 2L gradient contractions:
+//   repeat L: g = -(q P); p = (e/2) g + p; q = e p + q; g = -(q P); p = (e/2) g + p
+// Every update is the reference's separate IEEE multiply then add (axpy,
+// runtime.py:253-255); e/2 is the reference's `div e 2.0`. Writes back
+// leapfrog.{q, p, g, i, _ret}; the block's terminator pops the pc (return).
+// op: in = {q, p, e}, out row = _ret, imm0 = target slot, imm1 = L,
+//     imm2 = loop-head block, bits = g_row | i_row << 32.
+__device__ inline void warp_leapfrog(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
+                                     long long chain) {
+  const int lane = threadIdx.x & 31;
+  const DevTarget& tg = a.targets[op.imm0];
+  const int d = tg.dim, steps = op.imm1;
+  const int SQ = lf_stride_q(d), SP = lf_stride_p(d);
+  double* Qs = sm;
+  double* Ps = sm + 8 * SQ;
+  double* Es = Ps + 8 * SP;
+  const int grow = (int)(op.bits & 0xffffffff), irow = (int)(op.bits >> 32);
+  __syncwarp();
+  const unsigned mask = __ballot_sync(kFull, part);
+  const int n = __popc(mask);
+  uint64_t* myq = part ? ln.row(op.in_row[0]) : nullptr;  // q, p, _ret are registers
+  uint64_t* myp = part ? ln.row(op.in_row[1]) : nullptr;
+  const double mye = part ? as_f64(ln.in(op, 2)[0]) : 0.0;
+  uint64_t* my_g = (part && grow >= 0) ? ln.row(grow) : nullptr;
+  uint64_t* my_ret = part ? ln.row(op.out_row) : nullptr;
+  if (part) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
+  if (part && a.lane_trace != nullptr) {  // the blocks a lane walks inside the function
+    const int head = op.imm2;
+    lane_trace_put(a, chain, head);
+    for (int i = 0; i < steps; ++i) {
+      lane_trace_put(a, chain, head + 1);
+      lane_trace_put(a, chain, head);
+    }
+    lane_trace_put(a, chain, head + 2);
+  }
+  for (int mt = 0; mt * 8 < n; ++mt) {
+    for (int r = 0; r < 8; ++r) {  // stage the m-tile's 8 chains (zero rows pad)
+      const int lr = mtile_lane(mask, n, mt, r);
+      const uint64_t* qg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, lr < 0 ? 0 : lr);
+      const uint64_t* pg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, lr < 0 ? 0 : lr);
+      const double er = __shfl_sync(kFull, mye, lr < 0 ? 0 : lr);
+      for (int k = lane; k < SQ; k += 32) Qs[r * SQ + k] = (lr >= 0 && k < d) ? as_f64(qg[(size_t)k * 32]) : 0.0;
+      for (int k = lane; k < SP; k += 32) Ps[r * SP + k] = (lr >= 0 && k < d) ? as_f64(pg[(size_t)k * 32]) : 0.0;
+      if (lane == 0) Es[r] = lr >= 0 ? er : 0.0;
+    }
+    __syncwarp();
+    const int g = lane >> 2;
+    const int src = mtile_lane(mask, n, mt, g);
+    const double half = __ddiv_rn(Es[g], 2.0);
+    uint64_t* gg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_g, src < 0 ? 0 : src);
+    auto a_at = [&](int k) -> double { return Qs[g * SQ + k]; };
+    for (int it = 0; it < steps; ++it) {
+      for (int hs = 0; hs < 2; ++hs) {
+        const bool last = (it == steps - 1) && hs == 1;
+        for (int nt0 = 0; nt0 < tg.NT1; nt0 += LSB_NT_CHUNK) {
+          const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
+          LSB_NT_DISPATCH(ntc, {
+            double acc[NTC][2];
+            lsb::mtile_gemm<NTC>(acc, tg.B1, tg.KS1, tg.NT1, nt0, a_at);
+            _Pragma("unroll")
+            for (int j = 0; j < NTC; ++j) {
+              const int col = 8 * (nt0 + j) + 2 * (lane & 3);
+              double2* pp = reinterpret_cast<double2*>(Ps + g * SP + col);
+              double2 pv = *pp;
+              const double g0 = -acc[j][0], g1 = -acc[j][1];
+              pv.x = __dadd_rn(__dmul_rn(half, g0), pv.x);
+              pv.y = __dadd_rn(__dmul_rn(half, g1), pv.y);
+              if (col + 1 < d) *pp = pv;
+              else if (col < d) Ps[g * SP + col] = pv.x;  // odd d: the pad column stays zero
+              if (last && src >= 0 && gg != nullptr) {
+                if (col < d) gg[(size_t)col * 32] = f64_bits(g0);
+                if (col + 1 < d) gg[(size_t)(col + 1) * 32] = f64_bits(g1);
+              }
+            }
+          });
+        }
+        __syncwarp();
+        if (hs == 0) {  // q = e p + q over the tile
+          for (int idx = lane; idx < 8 * d; idx += 32) {
+            const int r = idx / d, k = idx - r * d;
+            Qs[r * SQ + k] = __dadd_rn(__dmul_rn(Es[r], Ps[r * SP + k]), Qs[r * SQ + k]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    for (int r = 0; r < 8; ++r) {  // write back q, p and _ret = vcat(q, p)
+      const int lr = mtile_lane(mask, n, mt, r);
+      if (lr < 0) break;
+      uint64_t* qo = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, lr);
+      uint64_t* po = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, lr);
+      uint64_t* ro = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_ret, lr);
+      for (int k = lane; k < d; k += 32) {
+        const uint64_t qv = f64_bits(Qs[r * SQ + k]), pv = f64_bits(Ps[r * SP + k]);
+        qo[(size_t)k * 32] = qv;
+        po[(size_t)k * 32] = pv;
+        ro[(size_t)k * 32] = qv;
+        ro[(size_t)(d + k) * 32] = pv;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- one block step for one lane (both engines) ---------------------------------------------
+
+struct StepFault {
+  int pos = 0;  // op position + 1 (0 = none)
+  int kind = 0, var = 0, detail = 0;
+};
+
+// Execute block `b` for this lane (if active). WARP selects the warp-group
+// engine (cooperative DMMA ops and superblocks; every thread of the warp must
+// call). Returns true when the lane's pc reached the halt block.
+template <bool WARP>
+__device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int b, bool active,
+                                           long long chain, StepFault& f, double* lf_smem) {
+  const RBlock blk = a.blocks[b];
+  const ROp* ops = a.ops + blk.op_begin;
+  for (int k = 0; k < blk.op_count; ++k) {
+    const ROp& op = ops[k];
+    if (op.opcode == LS_OP_LEAPFROG) {
+      if (WARP) warp_leapfrog(a, ln, op, active && !f.pos, lf_smem, chain);
+      continue;
+    }
+    const bool coop = WARP && warp_coop(a, op);
+    if (!coop && (!active || f.pos)) continue;
+    bool part = active && !f.pos;
+    uint64_t* dst = nullptr;
+    bool push = false;
+    if (part) {
+      if (op.action == LS_POP) {
+        int& s = ln.sp_row(op.out_sp);
+        if (s < 1) f = StepFault{k + 1, LS_RUN_UNDERFLOW, op.out, 0};
+        else --s;
+        part = false;
+      } else if (op.out_sp >= 0) {
+        const int s = ln.sp_row(op.out_sp);
+        if (op.action == LS_PUSH) {
+          if (s >= a.depth) { f = StepFault{k + 1, LS_RUN_OVERFLOW, op.out, 0}; part = false; }
+          else { dst = ln.row(op.out_row + s * op.width); push = true; }
+        } else if (s < 1) {
+          f = StepFault{k + 1, LS_RUN_UNDERFLOW, op.out, 1};
+          part = false;
+        } else {
+          dst = ln.row(op.out_row + (s - 1) * op.width);
+        }
+      } else {
+        dst = ln.row(op.out_row);
+      }
+    }
+    if (coop) {
+      if (WARP) {
+        __syncwarp();
+        warp_gauss(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, op.opcode == LS_OP_LOGPDF);
+        __syncwarp();
+      }
+    } else if (part) {
+      compute_op(a, op, op.nin > 0 ? ln.in(op, 0) : nullptr, op.nin > 1 ? ln.in(op, 1) : nullptr,
+                 op.nin > 2 ? ln.in(op, 2) : nullptr, dst, ln.L);
+    }
+    if (part && push) ++ln.sp_row(op.out_sp);
+  }
+  if (!active || f.pos) return false;
+  int& psp = ln.sp_row(a.n_sp_rows - 1);
+  int* top = &ln.pcs[(psp - 1) * ln.L + ln.t];
+  switch (blk.term) {
+    case LS_JUMP: *top = blk.a; break;
+    case LS_BRANCH: *top = (ln.top(blk.cond_row, blk.cond_sp, blk.cond_w)[0] != 0) ? blk.a : blk.b; break;
+    case LS_PUSHJUMP:
+      *top = blk.b;
+      if (psp >= a.depth + 1) {
+        f = StepFault{blk.op_count + 1, LS_RUN_OVERFLOW, -1, 0};
+      } else {
+        ln.pcs[psp * ln.L + ln.t] = blk.a;
+        ++psp;
+      }
+      break;
+    default:
+      if (psp < 1) {
+        f = StepFault{blk.op_count + 1, LS_RUN_UNDERFLOW, -1, 0};
+      } else {
+        --psp;
+        if (psp >= 1 && ln.pcs[(psp - 1) * ln.L + ln.t] == a.halt) return true;
+      }
+      break;
+  }
+  return false;
+}
+
+}  // namespace lsbvm

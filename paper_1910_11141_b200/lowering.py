@@ -153,6 +153,83 @@ def fuse_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatProgram
     return ir.FlatProgram(tuple(blocks), flat.inputs, flat.output, flat.entry)
 
 
+# ---- superblocks ---------------------------------------------------------------------------
+
+
+def _is(op, out_cls, prim, ins=None):
+    if not isinstance(op, ir.Update) or op.prim.name != prim and not prim.endswith("*"):
+        return False
+    if prim.endswith("*") and not op.prim.name.startswith(prim[:-1]):
+        return False
+    return ins is None or tuple(op.inputs) == tuple(ins)
+
+
+def match_leapfrog(flat: ir.FlatProgram, classes: dict[str, str], grads: frozenset[str]) -> list[dict]:
+    """Find leapfrog functions of the NUTS-lite program (reference workloads.py:461-472).
+
+    Pattern, after demote_nonreentrant + fuse_copies (block indices b..b+3):
+      b  : i = const:i64:0                                   jump b+1
+      b+1: T1 = const:i64:L; T0 = lt i T1                    branch T0 b+2 b+3
+      b+2: g = grad q; T3 = 2.0; T2 = div e T3; p = axpy T2 g p; q = axpy e p q;
+           g = grad q; T5 = 2.0; T4 = div e T5; p = axpy T4 g p; T6 = 1; i = add i T6
+                                                             jump b+1
+      b+3: R = vcat q p                                      return
+    with q, p, e, i, R registers, and b+1..b+3 entered only from inside.
+    """
+    found = []
+    n = len(flat.blocks)
+    preds = [[] for _ in range(n + 1)]
+    for bi, blk in enumerate(flat.blocks):
+        for s in ir.flat_successors(blk.terminator):
+            preds[s].append(bi)
+    for b in range(n - 3):
+        b0, b1, b2, b3 = flat.blocks[b:b + 4]
+        try:
+            (o_i,) = b0.ops
+            if not (_is(o_i, None, "const:i64:0") and isinstance(b0.terminator, ir.FlatJump)
+                    and b0.terminator.target == b + 1):
+                continue
+            i = o_i.output
+            t1, t0 = b1.ops
+            if not (t1.prim.name.startswith("const:i64:") and _is(t0, None, "lt", (i, t1.output))):
+                continue
+            steps = int(t1.prim.name.split(":")[2])
+            tb = b1.terminator
+            if not (isinstance(tb, ir.FlatBranch) and tb.cond == t0.output
+                    and (tb.true_target, tb.false_target) == (b + 2, b + 3)):
+                continue
+            ops = b2.ops
+            if len(ops) != 11 or not (isinstance(b2.terminator, ir.FlatJump) and b2.terminator.target == b + 1):
+                continue
+            g1, c3, d2, ap1, aq, g2, c5, d4, ap2, c6, inc = ops
+            gname = g1.prim.name
+            q, gv = g1.inputs[0], g1.output
+            if gname not in grads or g2.prim.name != gname or g2.inputs != (q,) or g2.output != gv:
+                continue
+            p = ap1.output
+            e = d2.inputs[0]
+            ok = (c3.prim.name == "const:f64:2.0" and _is(d2, None, "div", (e, c3.output))
+                  and _is(ap1, None, "axpy", (d2.output, gv, p)) and _is(aq, None, "axpy", (e, p, q))
+                  and aq.output == q and c5.prim.name == "const:f64:2.0"
+                  and _is(d4, None, "div", (e, c5.output)) and _is(ap2, None, "axpy", (d4.output, gv, p))
+                  and ap2.output == p and c6.prim.name == "const:i64:1"
+                  and _is(inc, None, "add", (i, c6.output)) and inc.output == i)
+            if not ok:
+                continue
+            (r,) = b3.ops
+            if not (_is(r, None, "vcat", (q, p)) and isinstance(b3.terminator, ir.FlatReturn)):
+                continue
+            if any(classes.get(v) != "register" for v in (q, p, e, i, r.output)):
+                continue
+            if sorted(preds[b + 1]) != sorted([b, b + 2]) or preds[b + 2] != [b + 1] or preds[b + 3] != [b + 1]:
+                continue
+        except (ValueError, AttributeError, IndexError):
+            continue
+        found.append(dict(entry=b, head=b + 1, q=q, p=p, e=e, g=gv, i=i, ret=r.output,
+                          steps=steps, grad=gname))
+    return found
+
+
 # ---- table building ------------------------------------------------------------------------
 
 
@@ -348,18 +425,34 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
 
         for name, info in inst.items():
             add(name, "temporary", info["vt"], final_row(name))
-        new_blocks.append([dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]])
-                           for op in renamed])
+        out_ops = []
+        for op in renamed:
+            d = dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]])
+            if "refs" in op:  # superblock side outputs; dead temporaries are skipped (-1)
+                d["refs"] = [-1 if r in is_temp else index[r] for r in op["refs"]]
+            out_ops.append(d)
+        new_blocks.append(out_ops)
         new_conds.append(index[cond] if cond is not None else 0)
     return entries, new_blocks, new_conds, arena_base + arena_size
 
 
-def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool = True) -> DeviceProgram:
-    """Build the device tables for `compiled` given inferred lane types."""
+def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool = True,
+          superblocks: bool = False, max_superblock_dim: int = 256) -> DeviceProgram:
+    """Build the device tables for `compiled` given inferred lane types.
+
+    superblocks=True (warp-group engine only) replaces each recognised
+    leapfrog function entry with one fused LS_OP_LEAPFROG op + return.
+    """
     flat, classes = compiled.flat, dict(compiled.classes)
     if optimize:
         flat, classes = demote_nonreentrant(flat, classes, compiled.labels)
         flat = fuse_copies(flat, classes)
+    fused = {}
+    if optimize and superblocks:
+        for m in match_leapfrog(flat, classes, grad_names()):
+            t = resolve_kernel(m["grad"]).device.target
+            if t is not None and t.kind == 1 and t.dim <= max_superblock_dim:
+                fused[m["entry"]] = m
 
     grads = grad_names()
     for n in set(types):
@@ -377,6 +470,19 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     n_scratch = 0
     for bi, blk in enumerate(flat.blocks):
         ops: list[dict] = []
+        if bi in fused:
+            m = fused[bi]
+            t = resolve_kernel(m["grad"]).device.target
+            if t not in targets:
+                targets.append(t)
+            ops.append(dict(opcode=OPCODES["leapfrog"], action=ACTION_UPDATE, out=m["ret"],
+                            ins=[m["q"], m["p"], m["e"]], kind=0, width=2 * t.dim,
+                            imm0=targets.index(t), imm1=m["steps"], imm2=m["head"], bits=0,
+                            prim="$leapfrog", refs=[m["g"], m["i"]]))
+            terms.append((TERM_RETURN, 0, 0))
+            conds.append(None)
+            block_ops.append(ops)
+            continue
         for op in blk.ops:
             if isinstance(op, ir.Pop):
                 ops.append(dict(opcode=0, action=ACTION_POP, out=op.var, ins=[], kind=0, width=1,
@@ -435,9 +541,16 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
         begin = len(op_rows)
         for op in ops:
             ins = op["ins"] + [0] * (3 - len(op["ins"]))
+            bits = op["bits"]
+            if "refs" in op:  # superblock side outputs: g (or -1 when dead) | i << 32
+                gref, iref = op["refs"]
+                bits = (gref & 0xFFFFFFFF) | (iref << 32)
             op_rows.append((op["opcode"], op["action"], op["out"], len(op["ins"]), ins, op["kind"],
-                            op["width"], op["imm0"], op["imm1"], op["imm2"], op["bits"]))
+                            op["width"], op["imm0"], op["imm1"], op["imm2"], bits))
         g = sum(n for name, n in ref_prims[bi].items() if name in grads)
+        if bi in fused:  # the superblock performs every gradient of the function's L iterations
+            body = fused[bi]["entry"] + 2
+            g = fused[bi]["steps"] * sum(n for name, n in ref_prims[body].items() if name in grads)
         tt = terms[bi]
         block_rows.append((begin, len(op_rows) - begin, tt[0], tt[1], tt[2], dev_conds[bi], g, 0))
 

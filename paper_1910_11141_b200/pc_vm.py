@@ -196,6 +196,7 @@ class Machine:
         self.regs = _Views(self, "register")
         self.scratch = _Views(self, "temporary")
         self.halted = False
+        self.engine = "exact"
 
     @property
     def halt_index(self) -> int:
@@ -272,15 +273,34 @@ def _as_words(a: np.ndarray) -> np.ndarray:
     return a.view(np.uint64).reshape(a.shape[0], -1)
 
 
+ENGINES = ("auto", "exact", "cta", "warp")
+
+
+def _pick_engine(engine: str, z: int, lanes_per_group: int | None) -> str:
+    if engine not in ENGINES:
+        raise ValueError(f"unknown engine '{engine}' (one of {ENGINES})")
+    if engine != "auto":
+        return engine
+    if lanes_per_group is not None:
+        return "cta"
+    return "exact" if z <= MAX_GROUP_LANES else "warp"
+
+
 def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
                  trace: ScheduleTrace | None = None, schedule: str = "min_pc",
                  lanes_per_group: int | None = None, groups: int = 0,
                  optimize: bool = False, exact_logpdf: bool = True,
-                 lane_trace_cap: int = 0) -> Machine:
+                 lane_trace_cap: int = 0, engine: str = "auto") -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
     that slot; the pc stack gets depth+1 slots seeded [halt, entry].
+
+    engine: "exact" — all Z (<= 1024) lanes in one CTA group, reference min-pc
+    schedule, per-step trace, observers; "cta" — groups of `lanes_per_group`
+    lanes, one CTA each; "warp" — the throughput engine: one 32-lane group per
+    warp, DMMA target contractions, fused leapfrog superblocks (with
+    optimize); "auto" picks exact for Z <= 1024, else warp.
     """
     if mode not in ("masked", "gather"):
         raise ValueError(f"unknown mode '{mode}'")
@@ -290,19 +310,28 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     arrays = _prepare_inputs(flat, inputs)
     z = arrays[0].shape[0]
     types = infer_types(flat, [vtype_of(a) for a in arrays])
-    dp = lower(compiled, types, optimize=optimize)
+    kind = _pick_engine(engine, z, lanes_per_group)
+    if kind == "exact" and z > MAX_GROUP_LANES:
+        raise ValueError(f"the exact engine holds at most {MAX_GROUP_LANES} lanes")
+    dp = lower(compiled, types, optimize=optimize, superblocks=(kind == "warp"))
     program = _native.Program(dp)
-    exact = lanes_per_group is None and z <= MAX_GROUP_LANES
-    if lanes_per_group is None and not exact:
+    exact = kind == "exact"
+    if kind == "cta" and lanes_per_group is None:
         lanes_per_group = 256
+    lanes = z if exact else (32 if kind == "warp" else int(lanes_per_group))
     handle = _native.MachineHandle(program, z, depth, sched=schedule,
-                                   lanes_per_cta=0 if exact else int(lanes_per_group),
+                                   lanes_per_cta=int(lanes_per_group) if kind == "cta" else 0,
                                    ctas=groups, trace=exact and trace is not None,
-                                   exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap)
+                                   exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap,
+                                   warp_groups=(kind == "warp"))
     for k, a in enumerate(arrays):
         handle.set_input(k, _as_words(a))
-    lanes = z if exact else int(lanes_per_group)
-    return Machine(compiled, dp, handle, z, depth, mode, types, trace, schedule, exact, lanes)
+    m = Machine(compiled, dp, handle, z, depth, mode, types, trace, schedule, exact, lanes)
+    m.engine = kind
+    if not exact and trace is not None:
+        m.trace = GroupTrace("pc", z, compiled.labels, dp.block_prims, lanes,
+                             np.zeros(len(flat.blocks), np.int64), np.zeros(len(flat.blocks), np.int64))
+    return m
 
 
 def _raise_fault(m: Machine, st) -> None:
@@ -408,21 +437,16 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
         max_steps: int | None = DEFAULT_MAX_STEPS, observer=None, debug: bool = False,
         schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
         optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
-        return_machine: bool = False):
+        engine: str = "auto", return_machine: bool = False):
     """Execute a compiled program on the B200; returns (outputs, trace)."""
     arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
     z = arrays[0].shape[0] if arrays else 0
-    exact = lanes_per_group is None and z <= MAX_GROUP_LANES
     if optimize is None:
         optimize = observer is None and not debug
     tr: ScheduleTrace = ScheduleTrace(engine="pc", z=z)
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
-                     exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap)
-    if not exact:
-        m.trace = GroupTrace("pc", z, compiled.labels, m._dp.block_prims, m.lanes,
-                             np.zeros(len(compiled.flat.blocks), np.int64),
-                             np.zeros(len(compiled.flat.blocks), np.int64))
+                     exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine)
     out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
     if return_machine:
         return out, m.trace, m

@@ -106,6 +106,7 @@ OPCODES = {
     "vget": 26, "vstore": 27, "vcat": 28, "vfill": 29, "vslice": 30,
     "rng_uniform": 31,
     "logpdf": 32, "grad": 33,
+    "leapfrog": 64,  # fused superblock (lowering.match_leapfrog), never a source primitive
 }
 
 
