@@ -53,8 +53,12 @@ def parse():
     ap.add_argument("--dim", type=int, default=100)
     ap.add_argument("--iterations", type=int, default=10)
     ap.add_argument("--depth", type=int, default=10)
-    ap.add_argument("--lanes", type=int, default=128, help="lanes per schedule group (CTA)")
+    ap.add_argument("--engine", default="warp", choices=("warp", "cta"),
+                    help="warp: 32-lane group per warp + DMMA + superblocks; cta: CTA groups")
+    ap.add_argument("--lanes", type=int, default=128, help="lanes per CTA group (cta engine)")
     ap.add_argument("--groups", type=int, default=0, help="persistent CTAs (0 = auto)")
+    ap.add_argument("--exact-logpdf", action="store_true",
+                    help="numpy einsum summation order for logpdf (default: DMMA form, 1e-15 rel)")
     ap.add_argument("--schedule", default="min_pc", choices=("min_pc", "most_populated"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -192,7 +196,9 @@ def workload_config(args, target):
     return {"workload": f"NUTS-lite on {args.dim}-d correlated gaussian (rho=0.5, {target.name})",
             "chains_per_gpu": args.chains, "iterations": args.iterations, "max_tree_depth": args.depth,
             "step_size": 0.25, "leaf_steps": 4, "precision": "fp64",
-            "lanes_per_group": args.lanes, "schedule": args.schedule,
+            "engine": args.engine, "lanes_per_group": 32 if args.engine == "warp" else args.lanes,
+            "schedule": args.schedule,
+            "logpdf": "numpy einsum order" if args.exact_logpdf else "DMMA q.(Pq) (within 1e-15 rel)",
             "l2": "flushed between timed steps (256 MiB write); outputs exceed L2"}
 
 
@@ -222,10 +228,12 @@ def main():
     q0 = np.zeros((z, args.dim))
     key = chain_keys(first, z)
     types = infer_types(cp.flat, [vtype_of(q0), vtype_of(key)])
-    dp = lower(cp, types, optimize=True)
+    warp = args.engine == "warp"
+    dp = lower(cp, types, optimize=True, superblocks=warp)
     prog = _native.Program(dp)
     mach = _native.MachineHandle(prog, z, cfg.min_stack_depth, sched=args.schedule,
-                                 lanes_per_cta=args.lanes, ctas=args.groups, exact_logpdf=True)
+                                 lanes_per_cta=0 if warp else args.lanes, ctas=args.groups,
+                                 exact_logpdf=args.exact_logpdf, warp_groups=warp)
     # inputs resident in HBM before the timed region
     q0_d = torch.zeros((z, args.dim), dtype=torch.float64, device=dev)
     key_d = torch.from_numpy(key).to(dev)
@@ -284,8 +292,9 @@ def main():
         t0 = time.perf_counter()
         g_e2e = 0
         for _ in range(reps):
-            out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, lanes_per_group=args.lanes,
-                            groups=args.groups, schedule=args.schedule)
+            out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, engine=args.engine,
+                            lanes_per_group=None if warp else args.lanes, groups=args.groups,
+                            schedule=args.schedule, exact_logpdf=args.exact_logpdf)
             g_e2e += tr.useful_invocations({target.grad})
         dt = time.perf_counter() - t0
         if world > 1:

@@ -362,6 +362,7 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
 
         # --- views and in-place vcat chains
         owner: dict[str, tuple[str, int]] = {}   # instance -> (root owner, word offset)
+        chained: set[str] = set()                # instances that extend a vcat chain in place
 
         def root(n):
             return owner.get(n, (n, 0))
@@ -380,11 +381,19 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
                         inst[r]["end"] = max(inst[r]["end"], end)
             elif prim == "vcat":
                 a = op["ins"][0]
-                if a in inst and a not in owner and inst[a]["end"] == info["start"] \
-                        and op["ins"][1] != a and root(op["ins"][1])[0] != a:
-                    owner[name] = (a, 0)
-                    inst[a]["end"] = max(inst[a]["end"], end)
-                    inst[a]["span"] = max(inst[a].get("span", inst[a]["vt"].words), info["vt"].words)
+                # extend a's storage in place when a dies here and owns its rows (or is
+                # itself a chain member at offset 0 of a temporary's rows)
+                head = a
+                while head in owner and owner[head][1] == 0 and head in chained:
+                    head = owner[head][0]
+                if a in inst and (a not in owner or a in chained) and head in inst \
+                        and head not in owner and inst[a]["end"] == info["start"] \
+                        and op["ins"][1] != a and root(op["ins"][1])[0] not in (a, head):
+                    owner[name] = (head, 0)
+                    chained.add(name)
+                    inst[head]["end"] = max(inst[head]["end"], end)
+                    inst[head]["span"] = max(inst[head].get("span", inst[head]["vt"].words),
+                                             info["vt"].words)
         # the storage owner of every view / chain member must outlive it
         for name in owner:
             r = name
