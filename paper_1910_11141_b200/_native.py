@@ -1,8 +1,9 @@
 """ctypes binding of `include/lockstep_b200.h` (the C ABI of the B200 VM).
 
 This is the only place Python touches the CUDA library. It loads the
-in-tree `_lib/liblockstep_b200.so` and fails loudly (DeviceError) if the
-library or a GPU is missing: there is no CPU fallback behind it.
+in-tree `_lib/liblockstep_b200.so` (or a program-specialised build of the
+same ABI from `_lib/gen/`, see codegen.py) and fails loudly (DeviceError)
+if the library or a GPU is missing: there is no CPU fallback behind it.
 """
 
 from __future__ import annotations
@@ -46,8 +47,6 @@ class Status(C.Structure):
                 ("kernel_ms", C.c_double), ("launches", C.c_int64)]
 
 
-_lib = None
-
 _SIGS = {
     "ls_abi_version": ([], C.c_int),
     "ls_last_error": ([], C.c_char_p),
@@ -77,6 +76,8 @@ _SIGS = {
                         C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
 }
 
+_LIBS: dict[str, C.CDLL] = {}
+
 
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
@@ -84,26 +85,27 @@ def header_symbols() -> list[str]:
     return sorted(set(re.findall(r"^(?:int|const char\*)\s+(ls_\w+)\(", text, re.M)))
 
 
-def load():
-    """Load (never build) the CUDA library; DeviceError if it is absent."""
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not LIB_PATH.exists():
-        raise DeviceError(f"CUDA library {LIB_PATH} is missing; run "
+def load(path: Path | str | None = None) -> C.CDLL:
+    """Load (never build) a CUDA library of this ABI; DeviceError if it is absent."""
+    path = str(path or LIB_PATH)
+    lib = _LIBS.get(path)
+    if lib is not None:
+        return lib
+    if not Path(path).exists():
+        raise DeviceError(f"CUDA library {path} is missing; run "
                           "`python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = C.CDLL(str(LIB_PATH))
+    lib = C.CDLL(path)
     for name, (args, res) in _SIGS.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    _lib = lib
+    _LIBS[path] = lib
     return lib
 
 
-def _check(rc: int) -> None:
+def _check(rc: int, lib: C.CDLL | None = None) -> None:
     if rc != LS_OK:
-        msg = load().ls_last_error().decode(errors="replace")
+        msg = (lib or load()).ls_last_error().decode(errors="replace")
         if rc == LS_EINVAL:
             raise ValueError(msg)
         raise DeviceError(msg)
@@ -120,10 +122,11 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
 
 
 class Program:
-    """Owns an `ls_program` built from a DeviceProgram."""
+    """Owns an `ls_program` built from a DeviceProgram (in library `lib_path`)."""
 
-    def __init__(self, dp: DeviceProgram):
-        lib = load()
+    def __init__(self, dp: DeviceProgram, lib_path: Path | str | None = None):
+        self.lib = load(lib_path)
+        self.lib_path = str(lib_path or LIB_PATH)
         self.dp = dp
         self._keep = [np.ascontiguousarray(dp.blocks), np.ascontiguousarray(dp.ops),
                       np.ascontiguousarray(dp.vars), np.ascontiguousarray(dp.inputs, dtype=np.int32)]
@@ -132,7 +135,7 @@ class Program:
                            dp.flat.entry, _ptr(i) if len(i) else None, len(i), dp.output,
                            dp.flat_rows)
         h = C.c_void_p()
-        _check(lib.ls_program_create(C.byref(desc), C.byref(h)))
+        _check(self.lib.ls_program_create(C.byref(desc), C.byref(h)), self.lib)
         self.handle = h
         for slot, t in enumerate(dp.targets):
             self._bind(slot, t)
@@ -145,11 +148,12 @@ class Program:
         else:
             params, n, norm = t.params["sx"], t.params["sx"].shape[0], 0.0
         params = np.ascontiguousarray(params, dtype=np.float64)
-        _check(load().ls_program_bind_target(self.handle, slot, t.kind, t.dim, n, _ptr(params), norm))
+        _check(self.lib.ls_program_bind_target(self.handle, slot, t.kind, t.dim, n, _ptr(params), norm),
+               self.lib)
 
     def __del__(self):
-        if getattr(self, "handle", None) and _lib is not None:
-            _lib.ls_program_destroy(self.handle)
+        if getattr(self, "handle", None):
+            self.lib.ls_program_destroy(self.handle)
             self.handle = None
 
 
@@ -159,42 +163,45 @@ class MachineHandle:
     def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
                  lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
                  exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False):
-        lib = load()
         if sched not in SCHED:
             raise ValueError(f"unknown schedule '{sched}'")
         self.program = program
+        self.lib = program.lib
         self.z = z
         self.depth = depth
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
                            int(lane_trace_cap), int(warp_groups))
         self.lane_trace_cap = int(lane_trace_cap)
         h = C.c_void_p()
-        _check(lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)))
+        _check(self.lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)), self.lib)
         self.handle = h
+
+    def _c(self, rc):
+        _check(rc, self.lib)
 
     def set_input(self, idx: int, arr: np.ndarray) -> None:
         arr = np.ascontiguousarray(arr)
-        _check(load().ls_machine_set_input(self.handle, idx, _ptr(arr), arr.nbytes))
+        self._c(self.lib.ls_machine_set_input(self.handle, idx, _ptr(arr), arr.nbytes))
 
     def reset(self) -> None:
-        _check(load().ls_machine_reset(self.handle))
+        self._c(self.lib.ls_machine_reset(self.handle))
 
     def set_input_device(self, idx: int, dev_ptr: int, nbytes: int) -> None:
-        _check(load().ls_machine_set_input_device(self.handle, idx, C.c_void_p(dev_ptr), nbytes))
+        self._c(self.lib.ls_machine_set_input_device(self.handle, idx, C.c_void_p(dev_ptr), nbytes))
 
     def run(self, max_steps: int) -> Status:
         st = Status()
-        _check(load().ls_run(self.handle, max_steps, C.byref(st)))
+        self._c(self.lib.ls_run(self.handle, max_steps, C.byref(st)))
         return st
 
     def read_output(self, width: int, dtype) -> np.ndarray:
         out = np.empty((self.z, width), dtype=np.uint64)
-        _check(load().ls_read_output(self.handle, _ptr(out), out.nbytes))
+        self._c(self.lib.ls_read_output(self.handle, _ptr(out), out.nbytes))
         return out.view(dtype)
 
     def output_device_ptr(self) -> int:
         p = C.c_void_p()
-        _check(load().ls_output_device(self.handle, C.byref(p)))
+        self._c(self.lib.ls_output_device(self.handle, C.byref(p)))
         return p.value
 
     def fetch_trace(self, cap: int = 1 << 16) -> tuple[np.ndarray, np.ndarray]:
@@ -203,7 +210,7 @@ class MachineHandle:
             b = np.empty(cap, np.int32)
             a = np.empty(cap, np.int32)
             n = C.c_int64(0)
-            _check(load().ls_trace_fetch(self.handle, _ptr(b), _ptr(a), cap, C.byref(n)))
+            self._c(self.lib.ls_trace_fetch(self.handle, _ptr(b), _ptr(a), cap, C.byref(n)))
             blocks.append(b[:n.value])
             active.append(a[:n.value])
             if n.value < cap:
@@ -213,39 +220,39 @@ class MachineHandle:
     def block_totals(self, n_blocks: int) -> tuple[np.ndarray, np.ndarray]:
         s = np.zeros(n_blocks, np.int64)
         a = np.zeros(n_blocks, np.int64)
-        _check(load().ls_block_totals(self.handle, _ptr(s), _ptr(a)))
+        self._c(self.lib.ls_block_totals(self.handle, _ptr(s), _ptr(a)))
         return s, a
 
     def read_var(self, var: int, slots: int, width: int) -> np.ndarray:
         out = np.empty((slots, self.z, width), np.uint64)
-        _check(load().ls_read_var(self.handle, var, _ptr(out), out.nbytes))
+        self._c(self.lib.ls_read_var(self.handle, var, _ptr(out), out.nbytes))
         return out
 
     def read_pointers(self, var: int) -> np.ndarray:
         out = np.empty(self.z, np.int64)
-        _check(load().ls_read_pointers(self.handle, var, _ptr(out), self.z))
+        self._c(self.lib.ls_read_pointers(self.handle, var, _ptr(out), self.z))
         return out
 
     def read_pc_stack(self) -> np.ndarray:
         out = np.empty((self.depth + 1, self.z), np.int32)
-        _check(load().ls_read_pc_stack(self.handle, _ptr(out), out.size))
+        self._c(self.lib.ls_read_pc_stack(self.handle, _ptr(out), out.size))
         return out.astype(np.int64)
 
     def lane_traces(self) -> list[np.ndarray]:
         cap = self.lane_trace_cap
         blocks = np.empty((self.z, cap), np.int32)
         lens = np.empty(self.z, np.int32)
-        _check(load().ls_lane_trace_fetch(self.handle, _ptr(blocks), _ptr(lens), cap))
+        self._c(self.lib.ls_lane_trace_fetch(self.handle, _ptr(blocks), _ptr(lens), cap))
         if (lens > cap).any():
             raise ValueError(f"lane trace truncated: raise lane_trace_cap above {int(lens.max())}")
         return [blocks[i, :lens[i]].copy() for i in range(self.z)]
 
     def sync(self) -> None:
-        _check(load().ls_machine_sync(self.handle))
+        self._c(self.lib.ls_machine_sync(self.handle))
 
     def __del__(self):
-        if getattr(self, "handle", None) and _lib is not None:
-            _lib.ls_machine_destroy(self.handle)
+        if getattr(self, "handle", None):
+            self.lib.ls_machine_destroy(self.handle)
             self.handle = None
 
 

@@ -1,0 +1,398 @@
+"""Program-specialised block code for the warp engine (paper §5 "static blocks").
+
+The generic VM (`csrc/lsb_vm.cuh::exec_block`) interprets resolved op
+descriptors: every op pays a descriptor read, a dispatch and operand address
+arithmetic, and every scalar goes through HBM. This module partially
+evaluates a lowered program (`lowering.DeviceProgram`) into CUDA source with
+one function per flat block:
+
+* operand rows, widths and stack-pointer rows become constants;
+* block-local scalar temporaries become registers (never stored);
+* vector ops call the fixed-width helpers of `csrc/lsb_gen_rt.cuh`;
+* target contractions and the fused leapfrog superblock stay warp-cooperative
+  (every thread of the warp calls them, active or not).
+
+Semantics are exactly `exec_block<true>` (same arithmetic helpers, same
+fault rules, same terminators); tests compare both paths lane for lane.
+
+The generated header is compiled together with `csrc/engine.cu`
+(`-DLSB_GENERATED=...`) into `_lib/gen/liblockstep_b200_<hash>.so`, a full
+copy of the C ABI whose warp kernel dispatches to the generated blocks.
+Libraries are cached by content hash; `__graft_entry__.build()` pre-builds the
+benchmark program so nothing compiles on the GPU box.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from . import build as _build
+from .lowering import DeviceProgram
+from .runtime import OPCODES
+
+GEN_DIR = _build.LIB_DIR / "gen"
+OP = {v: k for k, v in OPCODES.items()}
+F64, I64, BOOL = 0, 1, 2
+STACKED, REGISTER, TEMPORARY = 0, 1, 2
+PUSH, UPDATE, POP = 0, 1, 2
+
+
+def _u64(bits: int) -> str:
+    return f"0x{int(bits) & 0xFFFFFFFFFFFFFFFF:016x}ull"
+
+
+class _Gen:
+    def __init__(self, dp: DeviceProgram):
+        self.dp = dp
+        self.vars = dp.vars
+        off, stk = 0, {}
+        for v in range(len(dp.vars)):
+            if dp.vars[v]["cls"] == STACKED:
+                stk[v] = off
+                off += int(dp.vars[v]["width"])
+        self.stk = stk
+        self.flat = int(dp.flat_rows)
+
+    # ---- operand access -----------------------------------------------------------------
+    def w(self, v):
+        return int(self.vars[v]["width"])
+
+    def cls(self, v):
+        return int(self.vars[v]["cls"])
+
+    def local(self, v, locals_):
+        return v in locals_
+
+    def base(self, v):
+        """Row expression of the variable's slot 0."""
+        if self.cls(v) == STACKED:
+            return f"({self.flat} + D * {self.stk[v]})"
+        return str(int(self.vars[v]["row"]))
+
+    def ptr(self, v):
+        """Pointer expression to the variable's current top (read)."""
+        if self.cls(v) == STACKED:
+            return f"ln.top({self.base(v)}, {int(self.vars[v]['sp'])}, {self.w(v)})"
+        return f"ln.row({self.base(v)})"
+
+    def scalar(self, v, locals_):
+        return f"s{v}" if v in locals_ else f"{self.ptr(v)}[0]"
+
+    # ---- one op -------------------------------------------------------------------------------
+    def op_code(self, k, op, locals_, pos):
+        """C++ statements for one non-cooperative op (inside `if (ok)`)."""
+        opc = int(op["opcode"])
+        act = int(op["action"])
+        out = int(op["out"])
+        nin = int(op["nin"])
+        ins = [int(x) for x in op["in"][:nin]]
+        name = OP.get(opc, "?")
+        lines = []
+        if act == POP:
+            sp = int(self.vars[out]["sp"])
+            lines += [f"{{ int& s_ = ln.sp_row({sp});",
+                      f"  if (s_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                      "  --s_; }"]
+            return lines
+        width = int(op["width"])
+        fk = int(op["kind"]) == F64
+        S = lambda j: self.scalar(ins[j], locals_)  # noqa: E731
+        P = lambda j: self.ptr(ins[j])  # noqa: E731
+        W = lambda j: self.w(ins[j])  # noqa: E731
+        # scalar expression forms
+        expr = None
+        if name == "const":
+            expr = _u64(op["bits"])
+        elif name == "id" and width == 1:
+            expr = S(0)
+        elif name in ("add", "sub", "mul", "div", "min", "max") and width == 1:
+            x, y = S(0), S(1)
+            if fk:
+                fn = {"add": "__dadd_rn", "sub": "__dsub_rn", "mul": "__dmul_rn", "div": "__ddiv_rn"}.get(name)
+                expr = (f"f64_bits({fn}(as_f64({x}), as_f64({y})))" if fn else
+                        f"f_min({x}, {y}, {'true' if name == 'min' else 'false'})")
+            else:
+                expr = {"add": f"({x} + {y})", "sub": f"({x} - {y})",
+                        "mul": f"(uint64_t)((unsigned long long)({x}) * (unsigned long long)({y}))",
+                        "div": f"i64_div({x}, {y})",
+                        "min": f"i_min({x}, {y}, true)", "max": f"i_min({x}, {y}, false)"}[name]
+        elif name in ("le", "lt", "eq"):
+            x, y = S(0), S(1)
+            c = {"le": "<=", "lt": "<", "eq": "=="}[name]
+            if fk:
+                expr = f"(uint64_t)(as_f64({x}) {c} as_f64({y}))"
+            elif name == "eq":
+                expr = f"(uint64_t)({x} == {y})"
+            else:
+                expr = f"(uint64_t)((int64_t)({x}) {c} (int64_t)({y}))"
+        elif name in ("and", "or"):
+            c = "&&" if name == "and" else "||"
+            expr = f"(uint64_t)(({S(0)} != 0) {c} ({S(1)} != 0))"
+        elif name == "not":
+            expr = f"(uint64_t)({S(0)} == 0)"
+        elif name == "neg" and width == 1:
+            expr = f"f64_bits(-as_f64({S(0)}))" if fk else f"(0ull - {S(0)})"
+        elif name == "abs" and width == 1:
+            expr = f"f64_bits(fabs(as_f64({S(0)})))" if fk else f"i_abs({S(0)})"
+        elif name in ("sqrt", "exp", "log", "sin", "cos", "floor") and width == 1:
+            fn = "__dsqrt_rn" if name == "sqrt" else name
+            expr = f"f64_bits({fn}(as_f64({S(0)})))"
+        elif name == "select" and width == 1:
+            expr = f"(({S(0)} != 0) ? {S(1)} : {S(2)})"
+        elif name == "vget":
+            expr = (f"({P(0)})[clip(to_i64({S(1)}, {str(self.vars[ins[1]]['kind'] == F64).lower()}), "
+                    f"{W(0)}) * S]")
+        elif name == "vslice" and width == 1:
+            expr = f"({P(0)})[{int(op['imm0'])} * S]"
+        elif name == "vfill" and width == 1:
+            expr = S(0)
+        elif name == "rng_uniform":
+            kf = str(self.vars[ins[0]]["kind"] == F64).lower()
+            cf = str(self.vars[ins[1]]["kind"] == F64).lower()
+            expr = f"f64_bits(lsb::rng_uniform(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf})))"
+        elif name == "dot":
+            expr = f"f64_bits(dot<{W(0)}>({P(0)}, {P(1)}))"
+        elif name == "logpdf":
+            expr = f"f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {P(0)}, S, a.exact_logpdf))"
+
+        if expr is not None and out in locals_:
+            return [f"s{out} = {expr};"]
+        # memory destination
+        dst, post = self.dst(out, act, width, pos)
+        lines += dst
+        if expr is not None:
+            lines.append(f"  d_[0] = {expr};")
+        elif name == "id":
+            lines.append(f"  copy<{width}>(d_, {P(0)});")
+        elif name == "vslice":
+            lines.append(f"  copy<{width}>(d_, {P(0)} + {int(op['imm0'])} * S);")
+        elif name == "vcat":
+            wa = W(0)
+            lines.append(f"  copy<{wa}>(d_, {P(0)});")
+            lines.append(f"  copy<{width - wa}>(d_ + {wa} * S, {P(1)});")
+        elif name == "vfill":
+            lines.append(f"  fill<{width}>(d_, {S(0)});")
+        elif name == "vstore":
+            kf = str(self.vars[ins[1]]["kind"] == F64).lower()
+            lines.append(f"  {{ const uint64_t v_ = {S(2)}; const int64_t k_ = clip(to_i64({S(1)}, {kf}), {width});")
+            lines.append(f"    copy<{width}>(d_, {P(0)}); d_[k_ * S] = v_; }}")
+        elif name == "axpy":
+            lines.append(f"  axpy<{width}>(d_, as_f64({S(0)}), {P(1)}, {P(2)});")
+        elif name == "select":
+            lines.append(f"  select<{width}>(d_, {S(0)} != 0, {P(1)}, {P(2)});")
+        elif name in ("add", "sub", "mul", "div", "min", "max"):
+            xs, ys = P(0), P(1)
+            if fk:
+                fn = {"add": "__dadd_rn", "sub": "__dsub_rn", "mul": "__dmul_rn", "div": "__ddiv_rn"}.get(name)
+                body = (f"f64_bits({fn}(as_f64(xs_[i * S]), as_f64(ys_[i * S])))" if fn else
+                        f"f_min(xs_[i * S], ys_[i * S], {'true' if name == 'min' else 'false'})")
+            else:
+                body = {"add": "xs_[i * S] + ys_[i * S]", "sub": "xs_[i * S] - ys_[i * S]",
+                        "mul": "(uint64_t)((unsigned long long)xs_[i * S] * (unsigned long long)ys_[i * S])",
+                        "div": "i64_div(xs_[i * S], ys_[i * S])",
+                        "min": "i_min(xs_[i * S], ys_[i * S], true)",
+                        "max": "i_min(xs_[i * S], ys_[i * S], false)"}[name]
+            lines.append(f"  {{ const uint64_t* xs_ = {xs}; const uint64_t* ys_ = {ys};")
+            lines.append(f"    ew<{width}>(d_, [&](int i) {{ return {body}; }}); }}")
+        elif name in ("neg", "abs", "sqrt", "exp", "log", "sin", "cos", "floor"):
+            if fk:
+                fn = {"neg": None, "abs": "fabs", "sqrt": "__dsqrt_rn"}.get(name, name)
+                body = "f64_bits(-as_f64(xs_[i * S]))" if name == "neg" else f"f64_bits({fn}(as_f64(xs_[i * S])))"
+            else:
+                body = "0ull - xs_[i * S]" if name == "neg" else "i_abs(xs_[i * S])"
+            lines.append(f"  {{ const uint64_t* xs_ = {P(0)}; ew<{width}>(d_, [&](int i) {{ return {body}; }}); }}")
+        elif name == "grad":
+            lines.append(f"  target_grad(a.targets[{int(op['imm0'])}], {P(0)}, S, d_);")
+        else:
+            raise NotImplementedError(f"codegen: opcode {opc} ({name})")
+        lines += post
+        lines.append("}")
+        return lines
+
+    def dst(self, out, act, width, pos):
+        """Open a `{ uint64_t* d_ = ...;` scope with stack checks; returns (lines, closing lines)."""
+        if self.cls(out) != STACKED:
+            return [f"{{ uint64_t* d_ = ln.row({self.base(out)});"], []
+        sp = int(self.vars[out]["sp"])
+        if act == PUSH:
+            return ([f"{{ int& sp_ = ln.sp_row({sp});",
+                     f"  if (sp_ >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                     f"  uint64_t* d_ = ln.row({self.base(out)} + sp_ * {width});"],
+                    ["  ++sp_;"])
+        return ([f"{{ const int sp_ = ln.sp_row({sp});",
+                 f"  if (sp_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 1}}; ok = false; goto {self.end}; }}",
+                 f"  uint64_t* d_ = ln.row({self.base(out)} + (sp_ - 1) * {width});"], [])
+
+    def coop_code(self, op, locals_, pos):
+        """A warp-cooperative op: every thread calls it; `ok` lanes participate."""
+        opc = int(op["opcode"])
+        name = OP.get(opc)
+        out = int(op["out"])
+        ins = [int(x) for x in op["in"][:int(op["nin"])]]
+        if name == "leapfrog":
+            bits = int(op["bits"])
+            gv = bits & 0xFFFFFFFF
+            gv = -1 if gv == 0xFFFFFFFF else gv
+            iv = bits >> 32
+            grow = self.base(gv) if gv >= 0 else "-1"
+            e = ins[2]
+            return [
+                "{ ROp lf_{};",
+                f"  lf_.in_row[0] = {self.base(ins[0])}; lf_.in_row[1] = {self.base(ins[1])};",
+                f"  lf_.in_row[2] = {self.base(e)}; lf_.in_sp[2] = {int(self.vars[e]['sp']) if self.cls(e) == STACKED else -1};",
+                f"  lf_.in_w[2] = 1; lf_.out_row = {self.base(out)};",
+                f"  lf_.imm0 = {int(op['imm0'])}; lf_.imm1 = {int(op['imm1'])}; lf_.imm2 = {int(op['imm2'])};",
+                f"  lf_.bits = (long long)(((unsigned long long)({grow}) & 0xffffffffull) | ((unsigned long long)({self.base(iv)}) << 32));",
+                "  warp_leapfrog(a, ln, lf_, ok, sm, chain); }",
+            ]
+        # gaussian grad / logpdf through DMMA
+        act = int(op["action"])
+        want_lp = name == "logpdf"
+        lines = ["{ bool part_ = ok; uint64_t* cd_ = nullptr;"]
+        if out in locals_:
+            raise NotImplementedError("cooperative op into a register-local scalar")
+        lines.append("  if (part_) {")
+        d, post = self.dst(out, act, int(op["width"]), pos)
+        # reuse dst() but without goto: faults here only clear part_
+        d = [s.replace(f"ok = false; goto {self.end};", "ok = false; part_ = false;") for s in d]
+        lines += ["    " + s for s in d]
+        lines.append("    if (part_) cd_ = d_; }")
+        lines.append("  }")
+        x = self.ptr(ins[0])
+        call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
+                f"{'true' if want_lp else 'false'});")
+        if want_lp:
+            lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
+            lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
+        else:
+            lines.append("  __syncwarp();")
+            lines.append(call)
+            lines.append("  __syncwarp();")
+        if post:  # push: advance the stack pointer of participating lanes
+            sp = int(self.vars[out]["sp"])
+            lines.append(f"  if (part_) ++ln.sp_row({sp});")
+        lines.append("}")
+        return lines
+
+    def is_coop(self, op):
+        name = OP.get(int(op["opcode"]))
+        if name == "leapfrog":
+            return True
+        if name in ("grad", "logpdf"):
+            t = self.dp.targets[int(op["imm0"])]
+            return t.kind == 1
+        return False
+
+    def block(self, b):
+        blk = self.dp.blocks[b]
+        ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
+        # scalar block-local temporaries -> registers
+        locals_ = set()
+        for op in ops:
+            if int(op["action"]) == POP:
+                continue
+            out = int(op["out"])
+            scalar_type = self.dp.types[self.dp.var_names[out]].width == 0  # f64[1] stays in memory
+            if self.cls(out) == TEMPORARY and scalar_type and not self.is_coop(op):
+                locals_.add(out)
+        for op in ops:  # an op that reads a coop output from memory keeps it in memory
+            if self.is_coop(op):
+                locals_.discard(int(op["out"]))
+        body = [f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane& ln, bool active, "
+                f"long long chain, StepFault& f, double* sm) {{",
+                "  const int D = a.depth; (void)D; (void)sm; (void)chain;",
+                "  bool ok = active;"]
+        if locals_:
+            body.append("  uint64_t " + ", ".join(f"s{v} = 0" for v in sorted(locals_)) + ";")
+        seg = 0
+        i = 0
+        while i < len(ops):
+            if self.is_coop(ops[i]):
+                body += ["  " + s for s in self.coop_code(ops[i], locals_, i + 1)]
+                i += 1
+                continue
+            self.end = f"seg{seg}_end"
+            body.append("  if (ok) {")
+            while i < len(ops) and not self.is_coop(ops[i]):
+                body += ["    " + s for s in self.op_code(i, ops[i], locals_, i + 1)]
+                i += 1
+            body.append("  }")
+            body.append(f"  {self.end}:;")
+            seg += 1
+        # terminator
+        term, ta, tb = int(blk["term"]), int(blk["a"]), int(blk["b"])
+        body.append("  if (!ok) return false;")
+        if term == 1:
+            c = int(blk["cond"])
+            body.append(f"  const bool cond_ = {self.scalar(c, locals_)} != 0;")
+        else:
+            body.append("  const bool cond_ = false;")
+        body.append(f"  return finish_block(a, ln, {term}, {ta}, {tb}, cond_, {int(blk['op_count']) + 1}, f);")
+        body.append("}")
+        return "\n".join(body)
+
+    def emit(self) -> str:
+        n = len(self.dp.blocks)
+        out = ["// generated by paper_1910_11141_b200/codegen.py — do not edit", "#pragma once",
+               '#include "lsb_gen_rt.cuh"', "namespace lsbgen {",
+               "__device__ __forceinline__ bool finish_block(const VMArgs& a, const Lane& ln, int term, int ta, int tb,",
+               "                                             bool cond, int pos, StepFault& f) {",
+               "  int& psp = ln.sp_row(a.n_sp_rows - 1);",
+               "  int* top = &ln.pcs[(psp - 1) * ln.L + ln.t];",
+               "  switch (term) {",
+               "    case LS_JUMP: *top = ta; return false;",
+               "    case LS_BRANCH: *top = cond ? ta : tb; return false;",
+               "    case LS_PUSHJUMP:",
+               "      *top = tb;",
+               "      if (psp >= a.depth + 1) { f = StepFault{pos, LS_RUN_OVERFLOW, -1, 0}; return false; }",
+               "      ln.pcs[psp * ln.L + ln.t] = ta; ++psp; return false;",
+               "    default:",
+               "      if (psp < 1) { f = StepFault{pos, LS_RUN_UNDERFLOW, -1, 0}; return false; }",
+               "      --psp;",
+               "      return psp >= 1 && ln.pcs[(psp - 1) * ln.L + ln.t] == a.halt;",
+               "  }",
+               "}"]
+        for b in range(n):
+            out.append(self.block(b))
+        out.append("__device__ __forceinline__ bool gen_exec_block(const VMArgs& a, const Lane& ln, int b, bool active,")
+        out.append("                                               long long chain, StepFault& f, double* sm) {")
+        out.append("  switch (b) {")
+        for b in range(n):
+            out.append(f"    case {b}: return gb_{b}(a, ln, active, chain, f, sm);")
+        out.append("  }")
+        out.append("  return false;")
+        out.append("}")
+        out.append("}  // namespace lsbgen")
+        return "\n".join(out) + "\n"
+
+
+def generate(dp: DeviceProgram) -> str:
+    """CUDA source of the program-specialised block functions."""
+    return _Gen(dp).emit()
+
+
+def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False) -> Path | None:
+    """Path of the specialised C-ABI library for `dp`; compiles it if missing and `build`."""
+    src = generate(dp)
+    h = hashlib.sha256((src + _build.source_digest()).encode()).hexdigest()[:16]
+    lib = GEN_DIR / f"liblockstep_b200_{h}.so"
+    if lib.exists():
+        return lib
+    if not build:
+        return None
+    GEN_DIR.mkdir(parents=True, exist_ok=True)
+    hdr = GEN_DIR / f"gen_{h}.cuh"
+    hdr.write_text(src)
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
+           f"-DLSB_GENERATED=\"{hdr}\"", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True, cwd=str(_build.ROOT))
+    os.replace(tmp, lib)
+    return lib

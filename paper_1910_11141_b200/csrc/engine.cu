@@ -31,6 +31,15 @@
 #include "../../include/lockstep_b200.h"
 #include "lsb_vm.cuh"
 
+// A program-specialised build (codegen.py) replaces the warp engine's block
+// interpreter with generated straight-line block functions.
+#ifdef LSB_GENERATED
+#include LSB_GENERATED
+#define LSB_WARP_EXEC(...) lsbgen::gen_exec_block(__VA_ARGS__)
+#else
+#define LSB_WARP_EXEC(...) exec_block<true>(__VA_ARGS__)
+#endif
+
 using namespace lsbvm;
 using lsb::as_f64;
 using lsb::f64_bits;
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(128, 4) vm_warp_kernel(const __grid_constant__
     const int count = __popc(__ballot_sync(kFull, active));
     if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
     StepFault f;
-    const bool halted_now = exec_block<true>(a, ln, b, active, *my_chain, f, my_smem);
+    const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, *my_chain, f, my_smem);
     const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
     const unsigned wmin = __reduce_min_sync(kFull, fkey);
     if (wmin != ~0u) {

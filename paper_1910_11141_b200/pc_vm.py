@@ -155,7 +155,13 @@ class GroupTrace(ScheduleTrace):
     def step_count(self) -> int:
         return int(self.block_steps.sum())
 
+    device_grads: np.ndarray | None = None  # per-block grads of the program the device ran
+    grad_names: frozenset = frozenset()
+
     def _per_block(self, counted):
+        if counted and self.device_grads is not None and set(counted) <= self.grad_names:
+            # fused superblocks move a function's gradients into its entry block
+            return self.device_grads.astype(np.int64)
         return np.array([sum(n for k, n in p.items() if counted is None or k in counted)
                          for p in self.block_prims], dtype=np.int64)
 
@@ -290,7 +296,8 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
                  trace: ScheduleTrace | None = None, schedule: str = "min_pc",
                  lanes_per_group: int | None = None, groups: int = 0,
                  optimize: bool = False, exact_logpdf: bool = True,
-                 lane_trace_cap: int = 0, engine: str = "auto") -> Machine:
+                 lane_trace_cap: int = 0, engine: str = "auto",
+                 codegen: bool | str = False) -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
@@ -301,6 +308,10 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     lanes, one CTA each; "warp" — the throughput engine: one 32-lane group per
     warp, DMMA target contractions, fused leapfrog superblocks (with
     optimize); "auto" picks exact for Z <= 1024, else warp.
+
+    codegen (warp engine): run program-specialised block code (codegen.py)
+    instead of the op interpreter; compiled once per program and cached
+    in-tree ("cached": use only a prebuilt library).
     """
     if mode not in ("masked", "gather"):
         raise ValueError(f"unknown mode '{mode}'")
@@ -314,7 +325,14 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     if kind == "exact" and z > MAX_GROUP_LANES:
         raise ValueError(f"the exact engine holds at most {MAX_GROUP_LANES} lanes")
     dp = lower(compiled, types, optimize=optimize, superblocks=(kind == "warp"))
-    program = _native.Program(dp)
+    lib = None
+    if codegen and kind == "warp":
+        from . import codegen as _cg
+
+        lib = _cg.library_for(dp, build=codegen != "cached")
+        if lib is None:
+            raise ValueError("no prebuilt specialised library for this program (codegen='cached')")
+    program = _native.Program(dp, lib)
     exact = kind == "exact"
     if kind == "cta" and lanes_per_group is None:
         lanes_per_group = 256
@@ -331,6 +349,10 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     if not exact and trace is not None:
         m.trace = GroupTrace("pc", z, compiled.labels, dp.block_prims, lanes,
                              np.zeros(len(flat.blocks), np.int64), np.zeros(len(flat.blocks), np.int64))
+        from .lowering import grad_names
+
+        m.trace.device_grads = np.array(dp.blocks["grads"])
+        m.trace.grad_names = grad_names()
     return m
 
 
@@ -437,7 +459,7 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
         max_steps: int | None = DEFAULT_MAX_STEPS, observer=None, debug: bool = False,
         schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
         optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
-        engine: str = "auto", return_machine: bool = False):
+        engine: str = "auto", codegen: bool | str = False, return_machine: bool = False):
     """Execute a compiled program on the B200; returns (outputs, trace)."""
     arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
     z = arrays[0].shape[0] if arrays else 0
@@ -446,7 +468,8 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
     tr: ScheduleTrace = ScheduleTrace(engine="pc", z=z)
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
-                     exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine)
+                     exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
+                     codegen=codegen)
     out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
     if return_machine:
         return out, m.trace, m

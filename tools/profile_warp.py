@@ -17,3 +17,8 @@ print(f"{st.kernel_ms:.1f} ms grads {st.useful_grads}", flush=True)
 tot_s, tot_a = m._h.block_totals(41)
 for b in np.argsort(-tot_s)[:12]:
     print(b, cp.labels[b], int(tot_s[b]), int(tot_a[b]), f"{tot_a[b] / max(tot_s[b], 1):.1f} lanes/step")
+ops_per_block = np.array([int(b["op_count"]) for b in m._dp.blocks])
+tot_ops = (tot_s * ops_per_block).sum()
+groups = max(1, (z + 31) // 32)
+print(f"ops executed per warp: {tot_ops / groups:.0f}; steps per warp {tot_s.sum() / groups:.0f}")
+print("top blocks by ops:", [(cp.labels[b], int(tot_s[b] * ops_per_block[b] / groups)) for b in np.argsort(-(tot_s * ops_per_block))[:8]])
