@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--exact-logpdf", action="store_true",
                     help="numpy einsum summation order for logpdf (default: DMMA form, 1e-15 rel)")
     ap.add_argument("--schedule", default="min_pc", choices=("min_pc", "most_populated"))
+    ap.add_argument("--no-codegen", action="store_true",
+                    help="warp engine with the op interpreter instead of specialised block code")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-chains", type=int, default=256)
@@ -196,7 +198,8 @@ def workload_config(args, target):
     return {"workload": f"NUTS-lite on {args.dim}-d correlated gaussian (rho=0.5, {target.name})",
             "chains_per_gpu": args.chains, "iterations": args.iterations, "max_tree_depth": args.depth,
             "step_size": 0.25, "leaf_steps": 4, "precision": "fp64",
-            "engine": args.engine, "lanes_per_group": 32 if args.engine == "warp" else args.lanes,
+            "engine": args.engine, "codegen": args.engine == "warp" and not args.no_codegen,
+            "lanes_per_group": 32 if args.engine == "warp" else args.lanes,
             "schedule": args.schedule,
             "logpdf": "numpy einsum order" if args.exact_logpdf else "DMMA q.(Pq) (within 1e-15 rel)",
             "l2": "flushed between timed steps (256 MiB write); outputs exceed L2"}
@@ -230,7 +233,12 @@ def main():
     types = infer_types(cp.flat, [vtype_of(q0), vtype_of(key)])
     warp = args.engine == "warp"
     dp = lower(cp, types, optimize=True, superblocks=warp)
-    prog = _native.Program(dp)
+    lib = None
+    if warp and not args.no_codegen:
+        from paper_1910_11141_b200 import codegen
+
+        lib = codegen.library_for(dp)  # prebuilt by __graft_entry__.build() for the default config
+    prog = _native.Program(dp, lib)
     mach = _native.MachineHandle(prog, z, cfg.min_stack_depth, sched=args.schedule,
                                  lanes_per_cta=0 if warp else args.lanes, ctas=args.groups,
                                  exact_logpdf=args.exact_logpdf, warp_groups=warp)
@@ -294,7 +302,8 @@ def main():
         for _ in range(reps):
             out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, engine=args.engine,
                             lanes_per_group=None if warp else args.lanes, groups=args.groups,
-                            schedule=args.schedule, exact_logpdf=args.exact_logpdf)
+                            schedule=args.schedule, exact_logpdf=args.exact_logpdf,
+                            codegen=warp and not args.no_codegen)
             g_e2e += tr.useful_invocations({target.grad})
         dt = time.perf_counter() - t0
         if world > 1:

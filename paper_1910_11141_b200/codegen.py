@@ -81,11 +81,27 @@ class _Gen:
         return f"ln.row({self.base(v)})"
 
     def scalar(self, v, locals_):
-        return f"s{v}" if v in locals_ else f"{self.ptr(v)}[0]"
+        if v in locals_:
+            return f"s{v}"
+        if self.cls(v) == REGISTER and self.w(v) == 1:
+            # register scalars are loaded once per segment and reused until written
+            if v not in self.cache:
+                self.pre.append(f"r{v} = {self.ptr(v)}[0];")
+                self.cache.add(v)
+                self.cached_vars.add(v)
+            return f"r{v}"
+        return f"{self.ptr(v)}[0]"
 
     # ---- one op -------------------------------------------------------------------------------
     def op_code(self, k, op, locals_, pos):
         """C++ statements for one non-cooperative op (inside `if (ok)`)."""
+        self.pre = []
+        lines = self._op_code(k, op, locals_, pos)
+        out = int(op["out"])
+        self.cache.discard(out)
+        return self.pre + lines
+
+    def _op_code(self, k, op, locals_, pos):
         opc = int(op["opcode"])
         act = int(op["action"])
         out = int(op["out"])
@@ -309,9 +325,12 @@ class _Gen:
                 "  bool ok = active;"]
         if locals_:
             body.append("  uint64_t " + ", ".join(f"s{v} = 0" for v in sorted(locals_)) + ";")
+        decl_at = len(body)
+        self.cached_vars = set()
         seg = 0
         i = 0
         while i < len(ops):
+            self.cache = set()  # memory may change across cooperative ops
             if self.is_coop(ops[i]):
                 body += ["  " + s for s in self.coop_code(ops[i], locals_, i + 1)]
                 i += 1
@@ -327,9 +346,12 @@ class _Gen:
         # terminator
         term, ta, tb = int(blk["term"]), int(blk["a"]), int(blk["b"])
         body.append("  if (!ok) return false;")
+        if self.cached_vars:
+            body.insert(decl_at, "  uint64_t " + ", ".join(f"r{v} = 0" for v in sorted(self.cached_vars)) + ";")
         if term == 1:
             c = int(blk["cond"])
-            body.append(f"  const bool cond_ = {self.scalar(c, locals_)} != 0;")
+            cv = f"s{c}" if c in locals_ else f"{self.ptr(c)}[0]"
+            body.append(f"  const bool cond_ = {cv} != 0;")
         else:
             body.append("  const bool cond_ = false;")
         body.append(f"  return finish_block(a, ln, {term}, {ta}, {tb}, cond_, {int(blk['op_count']) + 1}, f);")

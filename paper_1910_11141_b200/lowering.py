@@ -121,6 +121,122 @@ def demote_nonreentrant(flat: ir.FlatProgram, classes: dict[str, str], labels) -
     return ir.FlatProgram(tuple(blocks), flat.inputs, flat.output, flat.entry), new_classes
 
 
+def demote_unpushed(flat: ir.FlatProgram, classes: dict[str, str]) -> tuple:
+    """A stacked variable that is never pushed nor popped keeps pointer 1 forever:
+    its top is always slot 0, i.e. it is a register (e.g. `build_tree._ret`)."""
+    touched = set()
+    for blk in flat.blocks:
+        for op in blk.ops:
+            if isinstance(op, ir.Pop):
+                touched.add(op.var)
+            elif isinstance(op, ir.Push):
+                touched.add(op.output)
+    demoted = {v for v, c in classes.items() if c == "stacked" and v not in touched}
+    if not demoted:
+        return flat, classes
+    return flat, {v: ("register" if v in demoted else c) for v, c in classes.items()}
+
+
+def _op_liveness(flat: ir.FlatProgram):
+    """live-after sets per (block, op index) of the flat program (Pop reads and writes)."""
+    from .compiler import _flat_live_in
+
+    live_in = _flat_live_in(flat)
+    after: dict[tuple[int, int], set[str]] = {}
+    n = len(flat.blocks)
+    for bi, blk in enumerate(flat.blocks):
+        live: set[str] = set()
+        for s in ir.flat_successors(blk.terminator):
+            if 0 <= s < n:
+                live |= live_in[s]
+        if isinstance(blk.terminator, ir.FlatBranch):
+            live.add(blk.terminator.cond)
+        for oi in range(len(blk.ops) - 1, -1, -1):
+            op = blk.ops[oi]
+            after[(bi, oi)] = set(live)
+            if isinstance(op, ir.Pop):
+                live.add(op.var)
+            else:
+                live.discard(op.output)
+                live |= set(op.inputs)
+    return after
+
+
+def coalesce_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatProgram:
+    """Register copy coalescing: `update T = id R` with T defined only there and R
+    never redefined while T is live gives T == R over T's whole life, so T can be
+    renamed to R and the copy dropped (e.g. `build_tree.t1 = id build_tree._ret`)."""
+    keep = set(flat.inputs) | {flat.output}
+    defs: dict[str, list[tuple[int, int]]] = {}
+    for bi, blk in enumerate(flat.blocks):
+        for oi, op in enumerate(blk.ops):
+            if not isinstance(op, ir.Pop):
+                defs.setdefault(op.output, []).append((bi, oi))
+    after = _op_liveness(flat)
+    rename: dict[str, str] = {}
+
+    def rep(v):
+        while v in rename:
+            v = rename[v]
+        return v
+
+    for bi, blk in enumerate(flat.blocks):
+        for oi, op in enumerate(blk.ops):
+            if not (isinstance(op, ir.Update) and op.prim.name == "id"):
+                continue
+            t, r = op.output, op.inputs[0]
+            if t == r or t in keep or classes.get(t) != "register" or classes.get(r) != "register":
+                continue
+            if t in rename:
+                continue
+            # every definition of t must be a copy of the same r
+            if any(not (isinstance(flat.blocks[db].ops[do], ir.Update)
+                        and flat.blocks[db].ops[do].prim.name == "id"
+                        and flat.blocks[db].ops[do].inputs == (r,))
+                   for db, do in defs.get(t, ())):
+                continue
+            copies = set(defs.get(t, ()))
+            root = rep(r)
+            members = [root] + [v for v in rename if rep(v) == root]
+            ok = True
+            for m in members:
+                for (db, do) in defs.get(m, ()):
+                    if (db, do) in copies:
+                        continue
+                    if t in after[(db, do)]:
+                        ok = False
+                        break
+                if not ok:
+                    break
+            # t's own uses must not overlap a live interval of another class member
+            # that differs from r: only r's value flows into t, so the check above suffices
+            if ok:
+                rename[t] = r
+                defs.setdefault(root, []).extend(defs.get(t, ()))
+    if not rename:
+        return flat
+
+    def sub(v):
+        return rep(v)
+
+    blocks = []
+    for blk in flat.blocks:
+        ops = []
+        for op in blk.ops:
+            if isinstance(op, ir.Pop):
+                ops.append(ir.Pop(sub(op.var)))
+                continue
+            out, ins = sub(op.output), tuple(sub(v) for v in op.inputs)
+            if isinstance(op, ir.Update) and op.prim.name == "id" and ins == (out,):
+                continue  # the coalesced copy itself (a Push of v = id v is a real save)
+            ops.append(type(op)(out, op.prim, ins))
+        t = blk.terminator
+        if isinstance(t, ir.FlatBranch):
+            t = ir.FlatBranch(sub(t.cond), t.true_target, t.false_target)
+        blocks.append(ir.FlatBlock(tuple(ops), t))
+    return ir.FlatProgram(tuple(blocks), flat.inputs, flat.output, flat.entry)
+
+
 def fuse_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatProgram:
     """`update T = f(xs); update V = id T` (T temporary, single use) -> `update V = f(xs)`."""
     uses: dict[str, int] = {}
@@ -402,11 +518,36 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
             if r in inst:
                 inst[r]["end"] = max(inst[r]["end"], inst[name]["end"])
 
+        # --- chain sinks: a vcat chain whose last link writes a register V (that no
+        # other op of the chain's lifetime touches) is built directly in V's rows,
+        # so the final copy disappears (e.g. NUTS-lite's leaf/node packs into _ret)
+        sinks: dict[str, int] = {}
+        for k, op in enumerate(renamed):
+            v = op["out"]
+            if op["prim"] != "vcat" or v in inst or classes.get(v) != "register" or v not in index:
+                continue
+            a = op["ins"][0]
+            if a not in inst:
+                continue
+            r, off = a, 0
+            while r in owner:
+                off += owner[r][1]
+                r = owner[r][0]
+            if off != 0 or r not in inst or r in sinks or inst[r]["end"] != k:
+                continue
+            if any(v == o["out"] or v in o["ins"] for o in renamed[inst[r]["start"]:k]):
+                continue
+            if op["ins"][1] == v or root(op["ins"][1])[0] == r:
+                continue
+            sinks[r] = entries[index[v]][3]
+
         # --- arena allocation (first fit by start, closed intervals)
         live: list[tuple[int, int, int]] = []  # (end, offset, size)
         top = 0
         placed: dict[str, int] = {}
         for name, info in sorted(inst.items(), key=lambda kv: (kv[1]["start"], kv[0])):
+            if name in sinks:
+                continue
             if name in owner:
                 continue
             size = info.get("span", info["vt"].words)
@@ -430,6 +571,8 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
                 r = r2
             if r in placed:
                 return arena_base + placed[r] + off
+            if r in sinks:
+                return sinks[r] + off
             return entries[index[r]][3] + off
 
         for name, info in inst.items():
@@ -455,7 +598,9 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     flat, classes = compiled.flat, dict(compiled.classes)
     if optimize:
         flat, classes = demote_nonreentrant(flat, classes, compiled.labels)
+        flat, classes = demote_unpushed(flat, classes)
         flat = fuse_copies(flat, classes)
+        flat = coalesce_copies(flat, classes)
     fused = {}
     if optimize and superblocks:
         for m in match_leapfrog(flat, classes, grad_names()):

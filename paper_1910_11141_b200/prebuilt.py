@@ -1,0 +1,75 @@
+"""Programs whose specialised (codegen) libraries are built ahead of time.
+
+`__graft_entry__.build()` compiles these on the CPU builder so neither the
+GPU tests nor `bench.py` ever invoke nvcc on the GPU box. Each entry is the
+exact (program, input types, lowering options) the consumer uses, so the
+content hash in codegen.library_for matches.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .runtime import VType
+
+F64, I64 = VType("f64"), VType("i64")
+
+
+def nuts(dim: int, rho: float, **cfg):
+    from . import compile_program, compile_source, correlated_gaussian, nuts_lite_source
+    from .workloads import NutsConfig
+
+    config = NutsConfig(**cfg)
+    target = correlated_gaussian(dim, rho)
+    cp = compile_program(compile_source(nuts_lite_source(config, target), "nuts_main"))
+    return config, target, cp
+
+
+BENCH = dict(dim=100, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=10, iterations=10)
+# NUTS cases the GPU tests run through the specialised warp engine
+TEST_NUTS = [
+    dict(dim=2, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=6, iterations=20),
+    dict(dim=100, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=10, iterations=3),
+    dict(dim=5, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=8, iterations=4),
+]
+
+
+def specs():
+    """[(label, compiled, input types)] for every prebuilt specialised library."""
+    from . import compile_program, compile_source
+    from .workloads import corpus
+
+    out = []
+    for kw in [BENCH, *TEST_NUTS]:
+        kw = dict(kw)
+        dim, rho = kw.pop("dim"), kw.pop("rho")
+        _, _, cp = nuts(dim, rho, **kw)
+        out.append((f"nuts_d{dim}_T{kw['iterations']}", cp, [VType("f64", dim), I64]))
+    for e in corpus():
+        cp = compile_program(compile_source(e.source, e.entry))
+        ins = e.make_inputs(np.random.default_rng(0), 2)
+        from .runtime import vtype_of
+
+        out.append((e.name, cp, [vtype_of(a) for a in ins]))
+    return out
+
+
+def build_all(workers: int = 8, verbose: bool = False) -> list:
+    """Compile every prebuilt specialised library (in parallel); returns their paths."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import codegen
+    from .lowering import lower
+    from .pc_vm import infer_types
+
+    dps = [lower(cp, infer_types(cp.flat, ts), optimize=True, superblocks=True) for _, cp, ts in specs()]
+    with ThreadPoolExecutor(workers) as ex:
+        paths = list(ex.map(lambda dp: codegen.library_for(dp, verbose=verbose), dps))
+    keep = {p.name for p in paths}
+    for stale in codegen.GEN_DIR.glob("liblockstep_b200_*.so"):  # drop libraries of older sources
+        if stale.name not in keep:
+            stale.unlink()
+    for hdr in codegen.GEN_DIR.glob("gen_*.cuh"):
+        if f"liblockstep_b200_{hdr.stem[4:]}.so" not in keep:
+            hdr.unlink()
+    return paths

@@ -306,3 +306,39 @@ def test_sampler_statistics():
     cov = np.cov(samples.T)
     assert np.abs(mean).max() < 0.1
     assert np.abs(cov - t.cov).max() < 0.15
+
+
+# ---- warp engine: interpreter and program-specialised code (codegen) ------------------------
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_warp_engine_corpus_matches_oracle(corpus_compiled, codegen):
+    rng = np.random.default_rng(4)
+    for name, (e, _, cp) in corpus_compiled.items():
+        ins = e.make_inputs(rng, 77)
+        ref = oracle_run(cp, ins, 64).output
+        got, _ = L.run(cp, ins, depth=64, engine="warp", codegen=codegen)
+        assert_matches(got, ref, f"{name} codegen={codegen}")
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+@pytest.mark.parametrize("exact_logpdf", [True, False])
+def test_warp_engine_nuts_lanes_exact(codegen, exact_logpdf):
+    """Fused leapfrog superblocks + DMMA gradients: every lane's pc trace is the oracle's."""
+    from paper_1910_11141_b200 import prebuilt
+
+    for kw in prebuilt.TEST_NUTS:
+        kw = dict(kw)
+        cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+        z, d = 96, t.dim
+        ins = [np.zeros((z, d)), np.arange(z, dtype=np.int64) * 7919 + 11]
+        ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+        got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=codegen,
+                           exact_logpdf=exact_logpdf, lane_trace_cap=1 << 16, return_machine=True)
+        for lane, seq in enumerate(m.lane_traces()):
+            assert np.array_equal(seq, ref.lane_blocks[lane]), (d, lane)
+        assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
+        want = sum(a * 2 * cfg.leaf_steps for b, a in ref.steps if cp.labels[b] == "leapfrog.b2") \
+            // (2 * cfg.leaf_steps) * 2
+        assert tr.useful_invocations({t.grad}) == m.useful_grads > 0
+        assert m.useful_grads == want
