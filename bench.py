@@ -64,7 +64,7 @@ def parse():
                     help="warp engine with the op interpreter instead of specialised block code")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-chains", type=int, default=256)
+    ap.add_argument("--cpu-chains", type=int, default=1024)
     ap.add_argument("--cpu-iterations", type=int, default=10)
     return ap.parse_args()
 
@@ -87,9 +87,11 @@ def program(args):
 
 
 def chain_keys(first: int, count: int) -> np.ndarray:
-    """Unique per-chain keys (default_rng integers collide at 2^16+)."""
-    ids = np.arange(first, first + count, dtype=np.int64)
-    return (ids * 2654435761 + 12345) % (2**31 - 1)
+    """Unique per-chain keys (SURVEY.md §0.9: default_rng integers collide at 2^16+);
+    a key depends only on the global chain id, so sharding does not change any chain."""
+    from paper_1910_11141_b200.distributed import chain_keys as keys
+
+    return keys(first, first + count)
 
 
 class Clocks:
@@ -296,10 +298,12 @@ def main():
     # e2e through the public API with host buffers (H2D of inputs, D2H of chains inside)
     e2e = None
     if not args.no_e2e:
-        reps = max(1, min(args.steps, 2))
-        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
         g_e2e = 0
-        for _ in range(reps):
+        for i in range(reps + 1):  # the first call (lowering + device allocation) is warm-up
+            if i == 1:
+                t0 = time.perf_counter()
+                g_e2e = 0
             out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, engine=args.engine,
                             lanes_per_group=None if warp else args.lanes, groups=args.groups,
                             schedule=args.schedule, exact_logpdf=args.exact_logpdf,
@@ -325,6 +329,19 @@ def main():
                "sample": (f"oracle port of reference pc_vm.run (numpy), {target.name}, "
                           f"{args.cpu_chains} chains x {args.cpu_iterations} iterations, {dt_cpu:.1f}s")}
 
+    # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)
+    from paper_1910_11141_b200.distributed import diagnostics
+
+    chains_d = torch.empty((z, args.iterations, args.dim), dtype=torch.float64, device=dev)
+    mach.copy_output_to(chains_d.data_ptr(), chains_d.numel() * 8)
+    diag = diagnostics(chains_d[:, args.iterations // 2:] if args.iterations >= 4 else chains_d)
+    diag_summary = {"chains": diag.chains, "draws_per_chain": diag.draws,
+                    "rhat_max": float(np.max(diag.rhat)), "ess_min": float(np.min(diag.ess)),
+                    "mean_abs_max": float(np.max(np.abs(diag.mean))),
+                    "collective": "all_reduce of split-R-hat/ESS sufficient statistics"
+                                  + (" (NCCL)" if world > 1 else " (single rank)")}
+    del chains_d
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -333,7 +350,7 @@ def main():
             "data": "synthetic (q0=0, unique per-chain keys, random-free target parameters)",
             "config": {**workload_config(args, target), "parallelism": f"chains sharded over {world} GPU(s)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk,
+            "clocks": clk, "diagnostics": diag_summary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

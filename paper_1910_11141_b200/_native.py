@@ -63,6 +63,7 @@ _SIGS = {
     "ls_run": ([C.c_void_p, C.c_int64, C.POINTER(Status)], C.c_int),
     "ls_read_output": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_output_device": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "ls_copy_output_device": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "ls_block_totals": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "ls_read_var": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
@@ -198,6 +199,9 @@ class MachineHandle:
         out = np.empty((self.z, width), dtype=np.uint64)
         self._c(self.lib.ls_read_output(self.handle, _ptr(out), out.nbytes))
         return out.view(dtype)
+
+    def copy_output_to(self, dev_ptr: int, nbytes: int) -> None:
+        self._c(self.lib.ls_copy_output_device(self.handle, C.c_void_p(dev_ptr), nbytes))
 
     def output_device_ptr(self) -> int:
         p = C.c_void_p()

@@ -849,6 +849,14 @@ int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
   return LS_OK;
 }
 
+int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
+  if (!m || !dev_dst) return fail(LS_EINVAL, "null machine");
+  if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
+  CK(cudaMemcpyAsync(dev_dst, m->output, bytes, cudaMemcpyDeviceToDevice, m->stream));
+  CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
 int ls_output_device(ls_machine* m, void** dev) {
   if (!m || !dev) return fail(LS_EINVAL, "null machine");
   *dev = m->output;

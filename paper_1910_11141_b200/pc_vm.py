@@ -40,6 +40,9 @@ from .runtime import BOOL, I64, VType, batch, resolve_kernel, vtype_of
 
 DEFAULT_MAX_STEPS = 1_000_000
 MAX_GROUP_LANES = 1024
+# lowered programs (per compiled program and input types) and idle device machines
+_PROGRAM_CACHE: dict = {}
+_MACHINE_CACHE: dict = {}
 
 
 # ---- type inference (reference pc_vm.py:49-97) ----------------------------------------
@@ -297,7 +300,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
                  lanes_per_group: int | None = None, groups: int = 0,
                  optimize: bool = False, exact_logpdf: bool = True,
                  lane_trace_cap: int = 0, engine: str = "auto",
-                 codegen: bool | str = False) -> Machine:
+                 codegen: bool | str = False, reuse: bool = False) -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
@@ -324,24 +327,39 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     kind = _pick_engine(engine, z, lanes_per_group)
     if kind == "exact" and z > MAX_GROUP_LANES:
         raise ValueError(f"the exact engine holds at most {MAX_GROUP_LANES} lanes")
-    dp = lower(compiled, types, optimize=optimize, superblocks=(kind == "warp"))
-    lib = None
-    if codegen and kind == "warp":
-        from . import codegen as _cg
+    pkey = (id(compiled), tuple(map(str, (vtype_of(a) for a in arrays))), optimize, kind == "warp",
+            codegen if kind == "warp" else False)
+    hit = _PROGRAM_CACHE.get(pkey)
+    if hit is not None and hit[0] is compiled:
+        dp, program = hit[1], hit[2]
+    else:
+        dp = lower(compiled, types, optimize=optimize, superblocks=(kind == "warp"))
+        lib = None
+        if codegen and kind == "warp":
+            from . import codegen as _cg
 
-        lib = _cg.library_for(dp, build=codegen != "cached")
-        if lib is None:
-            raise ValueError("no prebuilt specialised library for this program (codegen='cached')")
-    program = _native.Program(dp, lib)
+            lib = _cg.library_for(dp, build=codegen != "cached")
+            if lib is None:
+                raise ValueError("no prebuilt specialised library for this program (codegen='cached')")
+        program = _native.Program(dp, lib)
+        if len(_PROGRAM_CACHE) >= 16:
+            _PROGRAM_CACHE.pop(next(iter(_PROGRAM_CACHE)))
+        _PROGRAM_CACHE[pkey] = (compiled, dp, program)
     exact = kind == "exact"
     if kind == "cta" and lanes_per_group is None:
         lanes_per_group = 256
     lanes = z if exact else (32 if kind == "warp" else int(lanes_per_group))
-    handle = _native.MachineHandle(program, z, depth, sched=schedule,
-                                   lanes_per_cta=int(lanes_per_group) if kind == "cta" else 0,
-                                   ctas=groups, trace=exact and trace is not None,
-                                   exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap,
-                                   warp_groups=(kind == "warp"))
+    mopts = dict(sched=schedule, lanes_per_cta=int(lanes_per_group) if kind == "cta" else 0,
+                 ctas=groups, trace=exact and trace is not None, exact_logpdf=exact_logpdf,
+                 lane_trace_cap=lane_trace_cap, warp_groups=(kind == "warp"))
+    mkey = (pkey, z, depth, tuple(sorted(mopts.items())))
+    handle = _MACHINE_CACHE.pop(mkey, None) if reuse else None
+    if handle is not None and handle.program is program:
+        handle.reset()
+    else:
+        handle = _native.MachineHandle(program, z, depth, **mopts)
+    if reuse:  # run() hands the machine back to the cache when it is done with it
+        handle.cache_key = mkey
     for k, a in enumerate(arrays):
         handle.set_input(k, _as_words(a))
     m = Machine(compiled, dp, handle, z, depth, mode, types, trace, schedule, exact, lanes)
@@ -466,11 +484,20 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
     if optimize is None:
         optimize = observer is None and not debug
     tr: ScheduleTrace = ScheduleTrace(engine="pc", z=z)
+    # device storage is reused across calls with the same program and shapes; a
+    # machine handed back to the caller (return_machine) is not recycled
+    reuse = not return_machine and observer is None and not debug
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
                      exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
-                     codegen=codegen)
-    out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
+                     codegen=codegen, reuse=reuse)
+    try:
+        out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
+    finally:
+        if reuse:
+            if len(_MACHINE_CACHE) >= 4:
+                _MACHINE_CACHE.pop(next(iter(_MACHINE_CACHE)))
+            _MACHINE_CACHE[m._h.cache_key] = m._h
     if return_machine:
         return out, m.trace, m
     return out, m.trace
