@@ -320,6 +320,9 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
         raise ValueError(f"unknown mode '{mode}'")
     if depth < 1:
         raise ValueError("stack depth must be at least 1")
+    from .compiler import adopt
+
+    compiled = adopt(compiled)  # also accepts programs built by the reference compiler
     flat = compiled.flat
     arrays = _prepare_inputs(flat, inputs)
     z = arrays[0].shape[0]
