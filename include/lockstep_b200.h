@@ -157,9 +157,13 @@ typedef struct {
   int32_t lane_trace_cap; /* >0: record each chain's block sequence (first cap steps) */
   int32_t warp_groups;    /* 1: throughput engine — every warp is a 32-lane group with
                              DMMA target contractions and fused superblocks; `ctas`
-                             then counts CTAs of 4 warps */
-  int32_t reserved[1];
+                             then caps the groups at 4 x ctas */
+  int32_t flags;          /* LS_MF_* bits                                             */
 } ls_machine_opts;
+
+/* ls_machine_opts.flags */
+#define LS_MF_NO_STAGE 1  /* warp engine: read target matrices from global memory
+                             instead of a per-CTA shared-memory copy */
 
 typedef struct {
   int32_t kind;           /* LS_RUN_*                                          */
@@ -208,6 +212,9 @@ int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes);
 int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap, int64_t* n);
 /* per-block totals over all groups: steps executed and sum of active lanes */
 int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active);
+/* warp engine: SM clock cycles each block's steps took, summed over groups (a
+   cycle-weighted profile of the program, complementary to ncu stall sampling) */
+int ls_block_cycles(ls_machine* m, int64_t* cycles);
 /* observer access (single-group machines): all `depth` slots of a var as
    host array [slots][z][width]; pointers as [z] int64 (stacked vars / -1 = pc) */
 int ls_read_var(ls_machine* m, int32_t var, void* host, int64_t bytes);

@@ -23,6 +23,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "lockstep_b200.h"
 LS_OK, LS_EINVAL, LS_ECUDA, LS_ENOMEM = 0, -1, -2, -3
 RUN_HALTED, RUN_PAUSED, RUN_OVERFLOW, RUN_UNDERFLOW, RUN_STEP_LIMIT = 0, 1, 2, 3, 4
 SCHED = {"min_pc": 0, "most_populated": 1}
+MF_NO_STAGE = 1  # ls_machine_opts.flags (lockstep_b200.h)
 
 
 class ProgramDesc(C.Structure):
@@ -37,7 +38,7 @@ class ProgramDesc(C.Structure):
 class MachineOpts(C.Structure):
     _fields_ = [("sched", C.c_int32), ("lanes_per_cta", C.c_int32), ("ctas", C.c_int32),
                 ("trace", C.c_int32), ("exact_logpdf", C.c_int32), ("lane_trace_cap", C.c_int32),
-                ("warp_groups", C.c_int32), ("reserved", C.c_int32 * 1)]
+                ("warp_groups", C.c_int32), ("flags", C.c_int32)]
 
 
 class Status(C.Structure):
@@ -66,6 +67,7 @@ _SIGS = {
     "ls_copy_output_device": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "ls_block_totals": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "ls_block_cycles": ([C.c_void_p, C.c_void_p], C.c_int),
     "ls_read_var": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_read_pointers": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_read_pc_stack": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
@@ -163,7 +165,8 @@ class MachineHandle:
 
     def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
                  lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
-                 exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False):
+                 exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False,
+                 stage_targets: bool = True):
         if sched not in SCHED:
             raise ValueError(f"unknown schedule '{sched}'")
         self.program = program
@@ -171,7 +174,7 @@ class MachineHandle:
         self.z = z
         self.depth = depth
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
-                           int(lane_trace_cap), int(warp_groups))
+                           int(lane_trace_cap), int(warp_groups), 0 if stage_targets else MF_NO_STAGE)
         self.lane_trace_cap = int(lane_trace_cap)
         h = C.c_void_p()
         _check(self.lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)), self.lib)
@@ -226,6 +229,11 @@ class MachineHandle:
         a = np.zeros(n_blocks, np.int64)
         self._c(self.lib.ls_block_totals(self.handle, _ptr(s), _ptr(a)))
         return s, a
+
+    def block_cycles(self, n_blocks: int) -> np.ndarray:
+        c = np.zeros(n_blocks, np.int64)
+        self._c(self.lib.ls_block_cycles(self.handle, _ptr(c)))
+        return c
 
     def read_var(self, var: int, slots: int, width: int) -> np.ndarray:
         out = np.empty((slots, self.z, width), np.uint64)

@@ -40,6 +40,14 @@ OP = {v: k for k, v in OPCODES.items()}
 F64, I64, BOOL = 0, 1, 2
 STACKED, REGISTER, TEMPORARY = 0, 1, 2
 PUSH, UPDATE, POP = 0, 1, 2
+# code-shape switches (part of the generated text, hence of the library hash)
+OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
+       "spcache": os.environ.get("LSB_CG_SPCACHE", "1") == "1",
+       "staged": os.environ.get("LSB_CG_STAGED", "0") == "1",
+       # B-fragment register double-buffering in mtile_gemm
+       "bpf": int(os.environ.get("LSB_CG_BPF", "0")),
+       # loads in flight per thread in the generated vector loops
+       "ewu": int(os.environ.get("LSB_CG_EWU", "16"))}
 
 
 def _u64(bits: int) -> str:
@@ -57,6 +65,11 @@ class _Gen:
                 off += int(dp.vars[v]["width"])
         self.stk = stk
         self.flat = int(dp.flat_rows)
+        self.in_seg = False
+        self.dirty: set[int] = set()
+        self.cache: set[int] = set()
+        self.cached_vars: set[int] = set()
+        self.pre: list[str] = []
 
     # ---- operand access -----------------------------------------------------------------
     def w(self, v):
@@ -77,8 +90,27 @@ class _Gen:
     def ptr(self, v):
         """Pointer expression to the variable's current top (read)."""
         if self.cls(v) == STACKED:
-            return f"ln.top({self.base(v)}, {int(self.vars[v]['sp'])}, {self.w(v)})"
+            r = int(self.vars[v]["sp"])
+            if self.in_seg:  # stack pointer cached in a register for the segment
+                return f"ln.row({self.base(v)} + (sp{r} > 0 ? sp{r} - 1 : 0) * {self.w(v)})"
+            return f"ln.top({self.base(v)}, {r}, {self.w(v)})"
         return f"ln.row({self.base(v)})"
+
+    def disjoint(self, dv, act, sv, d_off, s_off, w):
+        """Can a copy of w words from sv(+s_off) to dv(+d_off) use the no-alias helper?"""
+        if dv == sv:
+            return act == PUSH  # a push writes a fresh slot above the top it reads
+        if self.cls(dv) == STACKED or self.cls(sv) == STACKED:
+            return True  # distinct variables: stack regions never overlap other storage
+        d0 = int(self.vars[dv]["row"]) + d_off
+        s0 = int(self.vars[sv]["row"]) + s_off
+        return d0 + w <= s0 or s0 + w <= d0
+
+    def copy(self, w, dst_expr, src_expr, dv, act, sv, d_off=0, s_off=0):
+        if OPT["staged"] and w >= 16:
+            return f"  copy_staged<{w}>({dst_expr}, {src_expr}, sm);"
+        fn = "copy_nr" if OPT["noalias"] and self.disjoint(dv, act, sv, d_off, s_off, w) else "copy"
+        return f"  {fn}<{w}>({dst_expr}, {src_expr});"
 
     def scalar(self, v, locals_):
         if v in locals_:
@@ -111,9 +143,13 @@ class _Gen:
         lines = []
         if act == POP:
             sp = int(self.vars[out]["sp"])
-            lines += [f"{{ int& s_ = ln.sp_row({sp});",
-                      f"  if (s_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
-                      "  --s_; }"]
+            if not self.in_seg:
+                return [f"{{ int& s_ = ln.sp_row({sp});",
+                        f"  if (s_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                        "  --s_; }"]
+            self.dirty.add(sp)
+            lines += [f"if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                      f"--sp{sp};"]
             return lines
         width = int(op["width"])
         fk = int(op["kind"]) == F64
@@ -184,19 +220,20 @@ class _Gen:
         if expr is not None:
             lines.append(f"  d_[0] = {expr};")
         elif name == "id":
-            lines.append(f"  copy<{width}>(d_, {P(0)});")
+            lines.append(self.copy(width, "d_", P(0), out, act, ins[0]))
         elif name == "vslice":
-            lines.append(f"  copy<{width}>(d_, {P(0)} + {int(op['imm0'])} * S);")
+            lo = int(op["imm0"])
+            lines.append(self.copy(width, "d_", f"{P(0)} + {lo} * S", out, act, ins[0], 0, lo))
         elif name == "vcat":
             wa = W(0)
-            lines.append(f"  copy<{wa}>(d_, {P(0)});")
-            lines.append(f"  copy<{width - wa}>(d_ + {wa} * S, {P(1)});")
+            lines.append(self.copy(wa, "d_", P(0), out, act, ins[0]))
+            lines.append(self.copy(width - wa, f"d_ + {wa} * S", P(1), out, act, ins[1], wa, 0))
         elif name == "vfill":
             lines.append(f"  fill<{width}>(d_, {S(0)});")
         elif name == "vstore":
             kf = str(self.vars[ins[1]]["kind"] == F64).lower()
             lines.append(f"  {{ const uint64_t v_ = {S(2)}; const int64_t k_ = clip(to_i64({S(1)}, {kf}), {width});")
-            lines.append(f"    copy<{width}>(d_, {P(0)}); d_[k_ * S] = v_; }}")
+            lines.append("  " + self.copy(width, "d_", P(0), out, act, ins[0]).strip() + " d_[k_ * S] = v_; }")
         elif name == "axpy":
             lines.append(f"  axpy<{width}>(d_, as_f64({S(0)}), {P(1)}, {P(2)});")
         elif name == "select":
@@ -235,6 +272,14 @@ class _Gen:
         if self.cls(out) != STACKED:
             return [f"{{ uint64_t* d_ = ln.row({self.base(out)});"], []
         sp = int(self.vars[out]["sp"])
+        if self.in_seg:  # stack pointer cached in the segment's register sp<row>
+            if act == PUSH:
+                self.dirty.add(sp)
+                return ([f"{{ if (sp{sp} >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                         f"  uint64_t* d_ = ln.row({self.base(out)} + sp{sp} * {width});"],
+                        [f"  ++sp{sp};"])
+            return ([f"{{ if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 1}}; ok = false; goto {self.end}; }}",
+                     f"  uint64_t* d_ = ln.row({self.base(out)} + (sp{sp} - 1) * {width});"], [])
         if act == PUSH:
             return ([f"{{ int& sp_ = ln.sp_row({sp});",
                      f"  if (sp_ >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
@@ -280,7 +325,7 @@ class _Gen:
         lines.append("    if (part_) cd_ = d_; }")
         lines.append("  }")
         x = self.ptr(ins[0])
-        call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
+        call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], staged_B(a, {int(op['imm0'])}), part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
                 f"{'true' if want_lp else 'false'});")
         if want_lp:
             lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
@@ -327,27 +372,49 @@ class _Gen:
             body.append("  uint64_t " + ", ".join(f"s{v} = 0" for v in sorted(locals_)) + ";")
         decl_at = len(body)
         self.cached_vars = set()
+        all_sp: set[int] = set()
         seg = 0
         i = 0
         while i < len(ops):
             self.cache = set()  # memory may change across cooperative ops
             if self.is_coop(ops[i]):
+                self.in_seg = False
                 body += ["  " + s for s in self.coop_code(ops[i], locals_, i + 1)]
                 i += 1
                 continue
             self.end = f"seg{seg}_end"
+            j = i
+            while j < len(ops) and not self.is_coop(ops[j]):
+                j += 1
+            # stack pointers this segment touches: loaded once (in parallel), written back if moved
+            rows = set()
+            for op in ops[i:j]:
+                for v in [int(op["out"]), *[int(x) for x in op["in"][:int(op["nin"])]]]:
+                    if self.cls(v) == STACKED:
+                        rows.add(int(self.vars[v]["sp"]))
+            all_sp |= rows
+            self.in_seg, self.dirty = OPT["spcache"], set()
+            if not OPT["spcache"]:
+                rows = set()
+            body.append(f"  const bool ran{seg} = ok;")
             body.append("  if (ok) {")
-            while i < len(ops) and not self.is_coop(ops[i]):
+            body += [f"    sp{r} = ln.sp_row({r});" for r in sorted(rows)]
+            while i < j:
                 body += ["    " + s for s in self.op_code(i, ops[i], locals_, i + 1)]
                 i += 1
             body.append("  }")
             body.append(f"  {self.end}:;")
+            if self.dirty:
+                body.append(f"  if (ran{seg}) {{ " + " ".join(f"ln.sp_row({r}) = sp{r};" for r in sorted(self.dirty)) + " }")
+            self.in_seg = False
             seg += 1
         # terminator
         term, ta, tb = int(blk["term"]), int(blk["a"]), int(blk["b"])
         body.append("  if (!ok) return false;")
         if self.cached_vars:
             body.insert(decl_at, "  uint64_t " + ", ".join(f"r{v} = 0" for v in sorted(self.cached_vars)) + ";")
+        if all_sp:
+            body.insert(decl_at, "  int " + ", ".join(f"sp{r} = 0" for r in sorted(all_sp)) + ";")
         if term == 1:
             c = int(blk["cond"])
             cv = f"s{c}" if c in locals_ else f"{self.ptr(c)}[0]"
@@ -360,7 +427,9 @@ class _Gen:
 
     def emit(self) -> str:
         n = len(self.dp.blocks)
-        out = ["// generated by paper_1910_11141_b200/codegen.py — do not edit", "#pragma once",
+        out = ["// generated by paper_1910_11141_b200/codegen.py — do not edit",
+               f"// options: {sorted(OPT.items())}", "#pragma once",
+               f"#define LSB_GEN_STAGED {int(OPT['staged'])}",
                '#include "lsb_gen_rt.cuh"', "namespace lsbgen {",
                "__device__ __forceinline__ bool finish_block(const VMArgs& a, const Lane& ln, int term, int ta, int tb,",
                "                                             bool cond, int pos, StepFault& f) {",
@@ -412,7 +481,7 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     hdr.write_text(src)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
-           f"-DLSB_GENERATED=\"{hdr}\"", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
+           f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=str(_build.ROOT))

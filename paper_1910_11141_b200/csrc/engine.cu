@@ -197,20 +197,30 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
   }
 }
 
-__global__ void __launch_bounds__(128, 4) vm_warp_kernel(const __grid_constant__ VMArgs a) {
+// up to 16 warps per CTA (one CTA per SM when a target is staged); 128 registers
+constexpr int kWarpCtaMax = 16;
+__global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __grid_constant__ VMArgs a) {
   extern __shared__ double lf_smem[];
+  // stage the target's B fragments once per CTA; every warp's DMMA reads them at LDS latency
+  if (a.stage_doubles > 0) {
+    const double2* src = reinterpret_cast<const double2*>(a.stage_src);
+    double2* dst = reinterpret_cast<double2*>(lf_smem);
+    for (int i = threadIdx.x; i < a.stage_doubles / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (g >= a.n_groups) return;
   constexpr int L = 32;
   const Lane ln{a.ws + (size_t)g * a.group_rows * L, a.sp + (size_t)g * a.n_sp_rows * L,
                 a.pcs + (size_t)g * (a.depth + 1) * L, lane, L};
-  double* my_smem = lf_smem + (size_t)(threadIdx.x >> 5) * a.lf_smem_per_warp;
+  double* my_smem = lf_smem + a.stage_doubles + (size_t)(threadIdx.x >> 5) * a.lf_smem_per_warp;
   int* pc_sp = &ln.sp_row(a.n_sp_rows - 1);
   long long* my_chain = a.chain_of + (size_t)g * L + lane;
   long long steps = a.group_steps[g];
   long long* bsteps = a.blk_steps + (size_t)g * a.n_blocks;
   long long* bactive = a.blk_active + (size_t)g * a.n_blocks;
+  long long* bcycles = a.blk_cycles + (size_t)g * a.n_blocks;
   unsigned long long useful = 0, launched = 0;
   if (a.group_done[g]) return;
 
@@ -247,7 +257,9 @@ __global__ void __launch_bounds__(128, 4) vm_warp_kernel(const __grid_constant__
     const int count = __popc(__ballot_sync(kFull, active));
     if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
     StepFault f;
+    const long long t_start = clock64();
     const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, *my_chain, f, my_smem);
+    if (lane == 0) bcycles[b] += clock64() - t_start;
     const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
     const unsigned wmin = __reduce_min_sync(kFull, fkey);
     if (wmin != ~0u) {
@@ -391,6 +403,7 @@ struct ls_machine {
   long long* trace_n = nullptr;
   long long* blk_steps = nullptr;
   long long* blk_active = nullptr;
+  long long* blk_cycles = nullptr;
   FaultRec* fault = nullptr;
   int* flags = nullptr;  // [0] abort [1] paused-steps [2] paused-trace
   int* lane_trace = nullptr;
@@ -400,6 +413,9 @@ struct ls_machine {
   bool warp = false;
   bool refill = false;
   int lf_smem_per_warp = 0;
+  int warps_per_cta = 4;     // warp engine CTA shape
+  int stage_target = -1;     // target whose B fragments each CTA stages in shared memory
+  int stage_doubles = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long launches = 0;
@@ -472,10 +488,13 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   a.group_steps = m->group_steps; a.group_done = m->group_done;
   a.trace_block = m->trace_block; a.trace_active = m->trace_active;
   a.trace_cap = m->trace_cap; a.trace_n = m->trace_n;
-  a.blk_steps = m->blk_steps; a.blk_active = m->blk_active;
+  a.blk_steps = m->blk_steps; a.blk_active = m->blk_active; a.blk_cycles = m->blk_cycles;
   a.useful = m->counters + 1; a.launched = m->counters + 2;
   a.n_groups = m->groups;
   a.lf_smem_per_warp = m->lf_smem_per_warp;
+  a.stage_target = m->stage_target;
+  a.stage_doubles = m->stage_doubles;
+  a.stage_src = m->stage_target >= 0 ? p->targets[m->stage_target].B1 : nullptr;
   a.lane_trace = m->lane_trace; a.lane_trace_len = m->lane_trace_len; a.lane_trace_cap = m->lane_trace_cap;
   a.fault = m->fault; a.abort_flag = m->flags + 0; a.paused = m->flags + 1;
   return a;
@@ -580,7 +599,7 @@ int ls_machine_destroy(ls_machine* m) {
   cudaFree(m->d_input_ptrs); cudaFree(m->output); cudaFree(m->counters);
   cudaFree(m->group_steps); cudaFree(m->group_done); cudaFree(m->trace_block);
   cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
-  cudaFree(m->blk_active); cudaFree(m->fault); cudaFree(m->flags);
+  cudaFree(m->blk_active); cudaFree(m->blk_cycles); cudaFree(m->fault); cudaFree(m->flags);
   cudaFree(m->lane_trace); cudaFree(m->lane_trace_len);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
@@ -599,6 +618,7 @@ static int reset_state(ls_machine* m) {
   CK(cudaMemsetAsync(m->group_done, 0, m->groups * sizeof(int), m->stream));
   CK(cudaMemsetAsync(m->blk_steps, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
   CK(cudaMemsetAsync(m->blk_active, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
+  CK(cudaMemsetAsync(m->blk_cycles, 0, (size_t)m->groups * nb * sizeof(long long), m->stream));
   CK(cudaMemsetAsync(m->flags, 0, 4 * sizeof(int), m->stream));
   CK(cudaMemsetAsync(m->trace_n, 0, sizeof(long long), m->stream));
   if (m->lane_trace_len) CK(cudaMemsetAsync(m->lane_trace_len, 0, (size_t)m->z * sizeof(int), m->stream));
@@ -634,15 +654,51 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   m->warp = m->opts.warp_groups != 0;
   if (m->warp) {
     // one 32-lane group per warp, 4 warps per CTA; default: a group per 32 chains,
-    // capped at 16 resident warps per SM
+    // capped at the warps that are resident at once (persistent CTAs refill chains)
     m->lanes = 32;
-    const long long want = (z + 31) / 32;
-    groups = m->opts.ctas > 0 ? 4 * m->opts.ctas : (int)std::min<long long>(want, (long long)sms * 16);
-    if (groups > want) groups = (int)want;
     m->refill = true;
     for (const auto& op : p->ops)
       if (op.opcode == LS_OP_LEAPFROG)
         m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, lf_smem_doubles(p->targets[op.imm0].dim));
+#if defined(LSB_GENERATED) && LSB_GEN_STAGED
+    // generated block code stages long copies through 48 rows x 32 lanes per warp
+    m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 48 * 32);
+#endif
+    const long long want = (z + 31) / 32;
+    // Stage one gaussian target's B fragments per CTA when every superblock uses it:
+    // CTAs of up to 16 warps (one per SM) share the copy. Otherwise 4-warp CTAs.
+    int st = -1;
+    bool one = true;
+    for (const auto& op : p->ops)
+      if (op.opcode == LS_OP_LEAPFROG) {
+        if (st >= 0 && st != op.imm0) one = false;
+        st = op.imm0;
+      }
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (st >= 0 && one && !(m->opts.flags & LS_MF_NO_STAGE) && p->targets[st].kind == LS_TARGET_GAUSSIAN) {
+      const int sd = p->targets[st].KS1 * p->targets[st].NT1 * 32;
+      // enough warps per CTA that one CTA per SM covers the groups, 4..16
+      int wpc = (int)std::min<long long>(kWarpCtaMax, std::max<long long>(4, (want + sms - 1) / sms));
+      while (wpc >= 4 && ((size_t)sd + (size_t)wpc * m->lf_smem_per_warp) * sizeof(double) > (size_t)smem_optin) --wpc;
+      if (wpc >= 4) {
+        m->stage_target = st;
+        m->stage_doubles = sd;
+        m->warps_per_cta = wpc;
+      }
+    }
+    const size_t smem = ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vm_warp_kernel, 32 * m->warps_per_cta, smem) !=
+            cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    groups = m->opts.ctas > 0 ? 4 * m->opts.ctas
+                              : (int)std::min<long long>(want, (long long)sms * m->warps_per_cta * per_sm);
+    if (groups > want) groups = (int)want;
   } else {
     int lanes = m->opts.lanes_per_cta > 0 ? m->opts.lanes_per_cta : (int)std::min<long long>(z, kMaxLanes);
     if (m->opts.lanes_per_cta <= 0 && z > kMaxLanes) {
@@ -707,6 +763,7 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       (rc = dalloc(&m->group_done, groups)) ||
       (rc = dalloc(&m->blk_steps, (size_t)groups * p->blocks.size())) ||
       (rc = dalloc(&m->blk_active, (size_t)groups * p->blocks.size())) ||
+      (rc = dalloc(&m->blk_cycles, (size_t)groups * p->blocks.size())) ||
       (rc = dalloc(&m->fault, 1)) || (rc = dalloc(&m->flags, 4)) || (rc = dalloc(&m->trace_n, 1))) {
     ls_machine_destroy(m);
     return rc;
@@ -788,7 +845,7 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   ls_program* p = m->p;
   VMArgs a = make_args(m, max_steps);
   m->started = true;
-  size_t smem = m->warp ? (size_t)4 * m->lf_smem_per_warp * sizeof(double)
+  size_t smem = m->warp ? ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double)
                         : (p->blocks.size() + 1) * sizeof(int);
   if (smem > 48 * 1024) {
     if (m->warp) CK(cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -800,7 +857,8 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
     CK(cudaEventCreate(&m->ev1));
   }
   CK(cudaEventRecord(m->ev0, m->stream));
-  if (m->warp) vm_warp_kernel<<<(m->groups + 3) / 4, 128, smem, m->stream>>>(a);
+  if (m->warp)
+    vm_warp_kernel<<<(m->groups + m->warps_per_cta - 1) / m->warps_per_cta, 32 * m->warps_per_cta, smem, m->stream>>>(a);
   else vm_cta_kernel<<<m->groups, m->lanes, smem, m->stream>>>(a);
   CK(cudaGetLastError());
   CK(cudaEventRecord(m->ev1, m->stream));
@@ -901,6 +959,19 @@ int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active) {
     }
     steps[b] = ss;
     active[b] = aa;
+  }
+  return LS_OK;
+}
+
+int ls_block_cycles(ls_machine* m, int64_t* cycles) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  const size_t nb = m->p->blocks.size();
+  std::vector<long long> c((size_t)m->groups * nb);
+  CK(cudaMemcpy(c.data(), m->blk_cycles, c.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  for (size_t b = 0; b < nb; ++b) {
+    long long cc = 0;
+    for (int g = 0; g < m->groups; ++g) cc += c[(size_t)g * nb + b];
+    cycles[b] = cc;
   }
   return LS_OK;
 }

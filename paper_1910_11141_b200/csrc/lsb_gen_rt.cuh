@@ -19,17 +19,22 @@ using namespace lsbvm;
 
 constexpr int S = 32;  // lane stride of the warp engine
 
-// dst[i] = f(i) for i < W, 8 loads in flight before the stores
+#ifndef LSB_EW_UNROLL
+#define LSB_EW_UNROLL 16
+#endif
+constexpr int kEw = LSB_EW_UNROLL;
+
+// dst[i] = f(i) for i < W, kEw loads in flight before the stores
 template <int W, class F>
 __device__ __forceinline__ void ew(uint64_t* dst, const F& f) {
-  constexpr int full = W / 8 * 8;
+  constexpr int full = W / kEw * kEw;
 #pragma unroll 1
-  for (int i = 0; i < full; i += 8) {
-    uint64_t v[8];
+  for (int i = 0; i < full; i += kEw) {
+    uint64_t v[kEw];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = f(i + j);
+    for (int j = 0; j < kEw; ++j) v[j] = f(i + j);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) dst[(i + j) * S] = v[j];
+    for (int j = 0; j < kEw; ++j) dst[(i + j) * S] = v[j];
   }
 #pragma unroll
   for (int i = full; i < W; ++i) dst[i * S] = f(i);
@@ -38,6 +43,38 @@ __device__ __forceinline__ void ew(uint64_t* dst, const F& f) {
 template <int W>
 __device__ __forceinline__ void copy(uint64_t* dst, const uint64_t* src) {
   if (dst != src) ew<W>(dst, [&](int i) { return src[i * S]; });
+}
+
+// Copy between rows the generator proved disjoint: with __restrict__ and a static
+// width the compiler may hoist many loads ahead of the stores (memory-level
+// parallelism for the latency-bound packing copies).
+template <int W>
+__device__ __forceinline__ void copy_nr(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src) {
+#pragma unroll 32
+  for (int i = 0; i < W; ++i) dst[i * S] = src[i * S];
+}
+
+// Long copies through the warp's shared-memory staging area with cp.async
+// (LDGSTS): every thread issues all loads of a chunk for its own lane without
+// holding registers, waits once, then stores — one memory round trip per
+// chunk of CHUNK rows instead of one per 8 rows. Each thread only touches its
+// own lane's column of the staging area, so no warp synchronisation is needed.
+constexpr int kStageRows = 48;  // 48 rows x 32 lanes x 8 B = 12 KB per warp
+using lsb::cp_async8;
+using lsb::cp_async_wait_all;
+
+template <int W>
+__device__ __forceinline__ void copy_staged(uint64_t* dst, const uint64_t* src, double* sm) {
+  if (dst == src) return;
+  const int lane = threadIdx.x & 31;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(sm) + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < W; c0 += kStageRows) {
+    const int n = W - c0 < kStageRows ? W - c0 : kStageRows;
+    for (int i = 0; i < n; ++i) cp_async8(stage + i * S, src + (c0 + i) * S);
+    cp_async_wait_all();
+    for (int i = 0; i < n; ++i) dst[(c0 + i) * S] = stage[i * S];
+  }
 }
 
 template <int W>

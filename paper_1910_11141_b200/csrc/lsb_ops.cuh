@@ -22,6 +22,16 @@
 namespace lsb {
 
 __device__ __forceinline__ double as_f64(uint64_t w) { return __longlong_as_double((long long)w); }
+
+// asynchronous 8-byte global -> shared copy (LDGSTS): no register is held while in flight
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 __device__ __forceinline__ uint64_t f64_bits(double x) { return (uint64_t)__double_as_longlong(x); }
 
 // numpy float64 -> int64 cast on x86-64: truncation, and the "integer

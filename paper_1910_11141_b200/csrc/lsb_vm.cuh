@@ -97,10 +97,15 @@ struct VMArgs {
   long long* trace_n;
   long long* blk_steps;
   long long* blk_active;
+  long long* blk_cycles;        // [groups][n_blocks] SM clock cycles spent in each block
   unsigned long long* useful;
   unsigned long long* launched;
   int n_groups;
   int lf_smem_per_warp;
+  // warp engine: one target's B fragments staged in shared memory at offset 0
+  const double* stage_src;
+  int stage_doubles;            // 0 = nothing staged
+  int stage_target;
   int* lane_trace;
   int* lane_trace_len;
   int lane_trace_cap;
@@ -372,10 +377,28 @@ __device__ __forceinline__ int mtile_lane(unsigned mask, int n, int mt, int g) {
   return idx < n ? (int)__fns(mask, 0, idx + 1) : -1;
 }
 
+// The CTA's shared-memory copy of target `t`'s B fragments, or nullptr (warp engine).
+__device__ __forceinline__ const double* staged_B(const VMArgs& a, int t) {
+  extern __shared__ double lsb_dyn_smem[];
+  return (a.stage_doubles > 0 && t == a.stage_target) ? lsb_dyn_smem : nullptr;
+}
+
+template <bool SB>
+__device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bool part, const uint64_t* xp,
+                                       uint64_t* dst, bool want_logpdf);
+
 // grad, or fast logpdf, of a gaussian target for every participating lane of the
 // warp (lane-minor storage, stride 32). xp/dst: this lane's input and output.
-__device__ inline void warp_gauss(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
-                                  bool want_logpdf) {
+// Bs: the staged B fragments (staged_B) or nullptr.
+__device__ inline void warp_gauss(const DevTarget& tg, const double* Bs, bool part, const uint64_t* xp,
+                                  uint64_t* dst, bool want_logpdf) {
+  if (Bs) warp_gauss_impl<true>(tg, Bs, part, xp, dst, want_logpdf);
+  else warp_gauss_impl<false>(tg, tg.B1, part, xp, dst, want_logpdf);
+}
+
+template <bool SB>
+__device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bool part, const uint64_t* xp,
+                                       uint64_t* dst, bool want_logpdf) {
   const int lane = threadIdx.x & 31;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n = __popc(mask);
@@ -390,7 +413,7 @@ __device__ inline void warp_gauss(const DevTarget& tg, bool part, const uint64_t
       const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
       LSB_NT_DISPATCH(ntc, {
         double acc[NTC][2];
-        lsb::mtile_gemm<NTC>(acc, tg.B1, tg.KS1, tg.NT1, nt0, a_at);
+        lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, a_at);
         _Pragma("unroll")
         for (int j = 0; j < NTC; ++j) {
           _Pragma("unroll")
@@ -423,7 +446,128 @@ __device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
 // 128-bit) are bank-conflict free.
 __host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8 * 8; return s + ((12 - s % 16) + 16) % 16; }
 __host__ __device__ __forceinline__ int lf_stride_p(int d) { int s = (d + 7) / 8 * 8; return s + ((8 - s % 16) + 16) % 16; }
-__host__ __device__ __forceinline__ int lf_smem_doubles(int d) { return 8 * (lf_stride_q(d) + lf_stride_p(d)) + 8; }
+// d <= 128 uses the register-momentum superblock (only q staged in shared memory)
+constexpr int kLfRegMaxTiles = 16;
+__host__ __device__ __forceinline__ int lf_smem_doubles(int d) {
+  return (d + 7) / 8 <= kLfRegMaxTiles ? 8 * lf_stride_q(d) : 8 * (lf_stride_q(d) + lf_stride_p(d)) + 8;
+}
+
+// One accumulator pass (n-tiles C0 .. C0+7) of the register-momentum superblock:
+// g = -(q P) for the tile's 8 chains, p += (e/2) g in the C-fragment layout.
+template <int NT, int C0, bool SB>
+__device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
+                                        const double* Bf, double half, bool last, uint64_t* gg, int d) {
+  constexpr int NTC = (NT - C0) < 4 ? (NT - C0) : 4;  // 4 n-tiles per pass: p + acc fit in registers
+  const int lane = threadIdx.x & 31, g = lane >> 2;
+  double acc[NTC][2];
+  lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, C0, [&](int k) -> double { return Qs[g * SQ + k]; });
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double gv = -acc[j][e];
+      p[C0 + j][e] = __dadd_rn(__dmul_rn(half, gv), p[C0 + j][e]);
+      const int col = 8 * (C0 + j) + 2 * (lane & 3) + e;
+      if (last && gg != nullptr && col < d) gg[(size_t)col * 32] = f64_bits(gv);
+    }
+  }
+}
+
+// Register-momentum variant of the fused leapfrog superblock (d <= 128): p lives in
+// registers in the DMMA C-fragment layout, q in shared memory (A-fragment source).
+// Half the shared-memory footprint of the tile version, which leaves room for the
+// CTA-wide staged copy of the precision matrix's B fragments (Bf, SB = true).
+template <int NT, bool SB>
+__device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
+                                 long long chain, const double* Bf) {
+  const int lane = threadIdx.x & 31, g = lane >> 2;
+  const DevTarget& tg = a.targets[op.imm0];
+  const int d = tg.dim, steps = op.imm1;
+  const int SQ = lf_stride_q(d);
+  double* Qs = sm;
+  const int grow = (int)(op.bits & 0xffffffff), irow = (int)(op.bits >> 32);
+  __syncwarp();
+  const unsigned mask = __ballot_sync(kFull, part);
+  const int n = __popc(mask);
+  uint64_t* myq = part ? ln.row(op.in_row[0]) : nullptr;
+  uint64_t* myp = part ? ln.row(op.in_row[1]) : nullptr;
+  const double mye = part ? as_f64(ln.in(op, 2)[0]) : 0.0;
+  uint64_t* my_g = (part && grow >= 0) ? ln.row(grow) : nullptr;
+  uint64_t* my_ret = part ? ln.row(op.out_row) : nullptr;
+  if (part) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
+  if (part && a.lane_trace != nullptr) {
+    const int head = op.imm2;
+    lane_trace_put(a, chain, head);
+    for (int i = 0; i < steps; ++i) {
+      lane_trace_put(a, chain, head + 1);
+      lane_trace_put(a, chain, head);
+    }
+    lane_trace_put(a, chain, head + 2);
+  }
+  for (int mt = 0; mt * 8 < n; ++mt) {
+    for (int r = 0; r < 8; ++r) {  // stage q of the m-tile's 8 chains (zero rows pad)
+      const int lr = mtile_lane(mask, n, mt, r);
+      const uint64_t* qg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, lr < 0 ? 0 : lr);
+      for (int k = lane; k < SQ; k += 32) Qs[r * SQ + k] = (lr >= 0 && k < d) ? as_f64(qg[(size_t)k * 32]) : 0.0;
+    }
+    const int src = mtile_lane(mask, n, mt, g);
+    const int sl = src < 0 ? 0 : src;
+    const uint64_t* pg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, sl);
+    const double eg = __shfl_sync(kFull, mye, sl);
+    uint64_t* gg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_g, sl);
+    if (src < 0) gg = nullptr;
+    const double half = __ddiv_rn(eg, 2.0);
+    double p[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * nt + 2 * (lane & 3) + e;
+        p[nt][e] = (src >= 0 && col < d) ? as_f64(pg[(size_t)col * 32]) : 0.0;
+      }
+    __syncwarp();
+    for (int it = 0; it < steps; ++it) {
+      for (int hs = 0; hs < 2; ++hs) {
+        const bool last = (it == steps - 1) && hs == 1;
+        lf_kick<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        if constexpr (NT > 4) lf_kick<NT, 4, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        if constexpr (NT > 8) lf_kick<NT, 8, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        if constexpr (NT > 12) lf_kick<NT, 12, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        __syncwarp();
+        if (hs == 0) {  // drift: q = e p + q on this thread's (row, columns)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = 8 * nt + 2 * (lane & 3) + e;
+              if (col < d) Qs[g * SQ + col] = __dadd_rn(__dmul_rn(eg, p[nt][e]), Qs[g * SQ + col]);
+            }
+          __syncwarp();
+        }
+      }
+    }
+    // write back q, p and _ret = vcat(q, p): each thread its (row, columns)
+    uint64_t* qo = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, sl);
+    uint64_t* po = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, sl);
+    uint64_t* ro = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_ret, sl);
+    if (src >= 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * nt + 2 * (lane & 3) + e;
+          if (col < d) {
+            const uint64_t qv = f64_bits(Qs[g * SQ + col]), pv = f64_bits(p[nt][e]);
+            qo[(size_t)col * 32] = qv;
+            po[(size_t)col * 32] = pv;
+            ro[(size_t)col * 32] = qv;
+            ro[(size_t)(d + col) * 32] = pv;
+          }
+        }
+    }
+    __syncwarp();
+  }
+}
 
 // Fused leapfrog superblock: the whole `leapfrog(q, p, e)` function of the
 // NUTS-lite program (reference workloads.py:461-472; flat blocks
@@ -435,8 +579,33 @@ __host__ __device__ __forceinline__ int lf_smem_doubles(int d) { return 8 * (lf_
 // leapfrog.{q, p, g, i, _ret}; the block's terminator pops the pc (return).
 // op: in = {q, p, e}, out row = _ret, imm0 = target slot, imm1 = L,
 //     imm2 = loop-head block, bits = g_row | i_row << 32.
+template <bool SB>
+__device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
+                                   long long chain, const double* Bf);
+
 __device__ inline void warp_leapfrog(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                      long long chain) {
+  const DevTarget& tg = a.targets[op.imm0];
+  const double* Bs = staged_B(a, op.imm0);
+  switch (tg.NT1) {  // d <= 128: register-momentum variant
+#define LSB_LF_CASE(K)                                                         \
+  case K:                                                                      \
+    if (Bs) warp_leapfrog_rp<K, true>(a, ln, op, part, sm, chain, Bs);         \
+    else warp_leapfrog_rp<K, false>(a, ln, op, part, sm, chain, tg.B1);        \
+    return;
+    LSB_LF_CASE(1) LSB_LF_CASE(2) LSB_LF_CASE(3) LSB_LF_CASE(4) LSB_LF_CASE(5) LSB_LF_CASE(6)
+    LSB_LF_CASE(7) LSB_LF_CASE(8) LSB_LF_CASE(9) LSB_LF_CASE(10) LSB_LF_CASE(11) LSB_LF_CASE(12)
+    LSB_LF_CASE(13) LSB_LF_CASE(14) LSB_LF_CASE(15) LSB_LF_CASE(16)
+#undef LSB_LF_CASE
+    default: break;
+  }
+  if (Bs) warp_leapfrog_tile<true>(a, ln, op, part, sm, chain, Bs);
+  else warp_leapfrog_tile<false>(a, ln, op, part, sm, chain, tg.B1);
+}
+
+template <bool SB>
+__device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
+                                   long long chain, const double* Bf) {
   const int lane = threadIdx.x & 31;
   const DevTarget& tg = a.targets[op.imm0];
   const int d = tg.dim, steps = op.imm1;
@@ -486,7 +655,7 @@ __device__ inline void warp_leapfrog(const VMArgs& a, const Lane& ln, const ROp&
           const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
           LSB_NT_DISPATCH(ntc, {
             double acc[NTC][2];
-            lsb::mtile_gemm<NTC>(acc, tg.B1, tg.KS1, tg.NT1, nt0, a_at);
+            lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, a_at);
             _Pragma("unroll")
             for (int j = 0; j < NTC; ++j) {
               const int col = 8 * (nt0 + j) + 2 * (lane & 3);
@@ -582,7 +751,8 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
     if (coop) {
       if (WARP) {
         __syncwarp();
-        warp_gauss(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, op.opcode == LS_OP_LOGPDF);
+        warp_gauss(a.targets[op.imm0], staged_B(a, op.imm0), part, part ? ln.in(op, 0) : nullptr, dst,
+                   op.opcode == LS_OP_LOGPDF);
         __syncwarp();
       }
     } else if (part) {
