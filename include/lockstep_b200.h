@@ -89,6 +89,9 @@ enum ls_opcode {
   /* fused superblock: the whole leapfrog function (workloads.py:461-472)
      executed run-to-return for every selected lane; see DESIGN.md */
   LS_OP_LEAPFROG = 64,
+  /* push that only allocates the new top slot: a caller save whose copy is never
+     read (lowering.dead_saves); overflow-checked like any push */
+  LS_OP_ALLOC = 65,
 };
 
 /* ---- target kinds (workloads.correlated_gaussian / logistic_regression) ------ */

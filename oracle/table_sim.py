@@ -23,7 +23,7 @@ OPN = {1: "const", 2: "id", 3: "add", 4: "sub", 5: "mul", 6: "div", 7: "min", 8:
        10: "lt", 11: "eq", 12: "and", 13: "or", 14: "not", 15: "neg", 16: "abs", 17: "sqrt",
        18: "exp", 19: "log", 20: "sin", 21: "cos", 22: "floor", 23: "select", 24: "dot",
        25: "axpy", 26: "vget", 27: "vstore", 28: "vcat", 29: "vfill", 30: "vslice", 31: "rng_uniform",
-       32: "logpdf", 33: "grad"}
+       32: "logpdf", 33: "grad", 65: "alloc"}
 
 
 class Fault(Exception):
@@ -86,7 +86,7 @@ def run_lane(dp, inputs_words: list[np.ndarray], depth: int, max_steps: int = 10
                     raise Fault(("underflow", v))
                 sp[vars_[v]["sp"]] -= 1
                 continue
-            res = _compute(op, vec, vars_, targets, as_i64)
+            res = None if OPN[int(op["opcode"])] == "alloc" else _compute(op, vec, vars_, targets, as_i64)
             if vars_[v]["cls"] == 0:
                 r = vars_[v]["sp"]
                 if op["action"] == 0:
@@ -100,7 +100,8 @@ def run_lane(dp, inputs_words: list[np.ndarray], depth: int, max_steps: int = 10
                     base = var_row[v] + (sp[r] - 1) * vars_[v]["width"]
             else:
                 base = var_row[v]
-            ws[base:base + len(res)] = res
+            if res is not None:  # alloc: the new top slot is left as it was
+                ws[base:base + len(res)] = res
         t = blk["term"]
         if t == 0:
             pcs[-1] = int(blk["a"])

@@ -47,7 +47,9 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # B-fragment register double-buffering in mtile_gemm
        "bpf": int(os.environ.get("LSB_CG_BPF", "0")),
        # loads in flight per thread in the generated vector loops
-       "ewu": int(os.environ.get("LSB_CG_EWU", "16"))}
+       "ewu": int(os.environ.get("LSB_CG_EWU", "16")),
+       # dev-only superblock phase clocks (tools/sb_profile.py)
+       "sbprof": int(os.environ.get("LSB_CG_SBPROF", "0"))}
 
 
 def _u64(bits: int) -> str:
@@ -106,7 +108,17 @@ class _Gen:
         s0 = int(self.vars[sv]["row"]) + s_off
         return d0 + w <= s0 or s0 + w <= d0
 
+    def same_rows(self, dv, act, sv, d_off, s_off):
+        """Statically the same storage (an in-place chain link): the copy is a no-op."""
+        if act == PUSH:
+            return False
+        if self.cls(dv) == STACKED or self.cls(sv) == STACKED:
+            return dv == sv and d_off == s_off
+        return int(self.vars[dv]["row"]) + d_off == int(self.vars[sv]["row"]) + s_off
+
     def copy(self, w, dst_expr, src_expr, dv, act, sv, d_off=0, s_off=0):
+        if self.same_rows(dv, act, sv, d_off, s_off):
+            return "  /* in place */"
         if OPT["staged"] and w >= 16:
             return f"  copy_staged<{w}>({dst_expr}, {src_expr}, sm);"
         fn = "copy_nr" if OPT["noalias"] and self.disjoint(dv, act, sv, d_off, s_off, w) else "copy"
@@ -192,7 +204,9 @@ class _Gen:
         elif name == "abs" and width == 1:
             expr = f"f64_bits(fabs(as_f64({S(0)})))" if fk else f"i_abs({S(0)})"
         elif name in ("sqrt", "exp", "log", "sin", "cos", "floor") and width == 1:
-            fn = "__dsqrt_rn" if name == "sqrt" else name
+            # transcendental bodies are shared out-of-line calls: straight-line blocks
+            # with many of them (draw_normals) would otherwise overflow the i-cache
+            fn = {"sqrt": "__dsqrt_rn", "floor": "floor"}.get(name, f"ool_{name}")
             expr = f"f64_bits({fn}(as_f64({S(0)})))"
         elif name == "select" and width == 1:
             expr = f"(({S(0)} != 0) ? {S(1)} : {S(2)})"
@@ -217,6 +231,8 @@ class _Gen:
         # memory destination
         dst, post = self.dst(out, act, width, pos)
         lines += dst
+        if name == "alloc":  # unobserved save: allocate the slot, copy nothing
+            return lines + ["  (void)d_;"] + post + ["}"]
         if expr is not None:
             lines.append(f"  d_[0] = {expr};")
         elif name == "id":
@@ -254,7 +270,7 @@ class _Gen:
             lines.append(f"    ew<{width}>(d_, [&](int i) {{ return {body}; }}); }}")
         elif name in ("neg", "abs", "sqrt", "exp", "log", "sin", "cos", "floor"):
             if fk:
-                fn = {"neg": None, "abs": "fabs", "sqrt": "__dsqrt_rn"}.get(name, name)
+                fn = {"neg": None, "abs": "fabs", "sqrt": "__dsqrt_rn", "floor": "floor"}.get(name, f"ool_{name}")
                 body = "f64_bits(-as_f64(xs_[i * S]))" if name == "neg" else f"f64_bits({fn}(as_f64(xs_[i * S])))"
             else:
                 body = "0ull - xs_[i * S]" if name == "neg" else "i_abs(xs_[i * S])"
@@ -289,6 +305,11 @@ class _Gen:
                  f"  if (sp_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 1}}; ok = false; goto {self.end}; }}",
                  f"  uint64_t* d_ = ln.row({self.base(out)} + (sp_ - 1) * {width});"], [])
 
+    def leapfrog_fn(self, t: int) -> str:
+        """The superblock instance for target slot t (its n-tile count is static here)."""
+        nt = (int(self.dp.targets[t].dim) + 7) // 8
+        return f"warp_leapfrog_nt<{nt}>" if nt <= 16 else "warp_leapfrog"
+
     def coop_code(self, op, locals_, pos):
         """A warp-cooperative op: every thread calls it; `ok` lanes participate."""
         opc = int(op["opcode"])
@@ -309,7 +330,7 @@ class _Gen:
                 f"  lf_.in_w[2] = 1; lf_.out_row = {self.base(out)};",
                 f"  lf_.imm0 = {int(op['imm0'])}; lf_.imm1 = {int(op['imm1'])}; lf_.imm2 = {int(op['imm2'])};",
                 f"  lf_.bits = (long long)(((unsigned long long)({grow}) & 0xffffffffull) | ((unsigned long long)({self.base(iv)}) << 32));",
-                "  warp_leapfrog(a, ln, lf_, ok, sm, chain); }",
+                f"  {self.leapfrog_fn(int(op['imm0']))}(a, ln, lf_, ok, sm, chain); }}",
             ]
         # gaussian grad / logpdf through DMMA
         act = int(op["action"])
@@ -326,7 +347,7 @@ class _Gen:
         lines.append("  }")
         x = self.ptr(ins[0])
         call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], staged_B(a, {int(op['imm0'])}), part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
-                f"{'true' if want_lp else 'false'});")
+                f"{'true' if want_lp else 'false'}, sm, a.lf_smem_per_warp);")
         if want_lp:
             lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
             lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
@@ -481,7 +502,8 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     hdr.write_text(src)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
-           f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
+           f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}",
+           f"-DLSB_SB_PROFILE={OPT['sbprof']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=str(_build.ROOT))

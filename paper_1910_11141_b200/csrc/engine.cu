@@ -657,9 +657,14 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     // capped at the warps that are resident at once (persistent CTAs refill chains)
     m->lanes = 32;
     m->refill = true;
-    for (const auto& op : p->ops)
+    for (const auto& op : p->ops) {
       if (op.opcode == LS_OP_LEAPFROG)
         m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, lf_smem_doubles(p->targets[op.imm0].dim));
+      // DMMA gradients / fast logpdfs stage their A operand as one 8-chain tile
+      if ((op.opcode == LS_OP_GRAD || op.opcode == LS_OP_LOGPDF) &&
+          p->targets[op.imm0].kind == LS_TARGET_GAUSSIAN && p->targets[op.imm0].NT1 <= kLfRegMaxTiles)
+        m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 8 * lf_stride_q(p->targets[op.imm0].dim));
+    }
 #if defined(LSB_GENERATED) && LSB_GEN_STAGED
     // generated block code stages long copies through 48 rows x 32 lanes per warp
     m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 48 * 32);
@@ -962,6 +967,17 @@ int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active) {
   }
   return LS_OK;
 }
+
+#if LSB_SB_PROFILE
+// dev-only: read and clear the superblock phase clocks (lsb_vm.cuh lsb_sb_prof)
+int ls_debug_sb_profile(uint64_t* out8) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out8, lsbvm::lsb_sb_prof, 8 * sizeof(uint64_t)));
+  static const uint64_t zero[8] = {0};
+  CK(cudaMemcpyToSymbol(lsbvm::lsb_sb_prof, zero, sizeof(zero)));
+  return LS_OK;
+}
+#endif
 
 int ls_block_cycles(ls_machine* m, int64_t* cycles) {
   if (!m) return fail(LS_EINVAL, "null machine");

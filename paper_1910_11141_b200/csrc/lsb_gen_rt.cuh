@@ -77,6 +77,12 @@ __device__ __forceinline__ void copy_staged(uint64_t* dst, const uint64_t* src, 
   }
 }
 
+// out-of-line libdevice transcendentals (same results as the inline calls)
+__device__ __noinline__ double ool_exp(double x) { return exp(x); }
+__device__ __noinline__ double ool_log(double x) { return log(x); }
+__device__ __noinline__ double ool_sin(double x) { return sin(x); }
+__device__ __noinline__ double ool_cos(double x) { return cos(x); }
+
 template <int W>
 __device__ __forceinline__ void fill(uint64_t* dst, uint64_t v) {
   ew<W>(dst, [&](int) { return v; });
@@ -93,9 +99,28 @@ __device__ __forceinline__ void select(uint64_t* dst, bool c, const uint64_t* x,
   if (src != dst) ew<W>(dst, [&](int i) { return src[i * S]; });
 }
 
+// (x*y).sum(): numpy's pairwise order (lsb_ops.cuh pairwise). For a static
+// W <= 128 the whole sum is unrolled so the loads can all be issued early.
 template <int W>
 __device__ __forceinline__ double dot(const uint64_t* x, const uint64_t* y) {
-  return lsb::dot_lane(x, y, W, S);
+  if constexpr (W < 8 || W > 128) {
+    return lsb::dot_lane(x, y, W, S);
+  } else {
+    auto p = [&](int i) { return __dmul_rn(as_f64(x[i * S]), as_f64(y[i * S])); };
+    constexpr int stop = W - W % 8;
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = p(j);
+#pragma unroll
+    for (int i = 8; i < stop; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], p(i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = stop; i < W; ++i) res = __dadd_rn(res, p(i));
+    return __dadd_rn(0.0, res);
+  }
 }
 
 __device__ __forceinline__ int64_t to_i64(uint64_t w, bool is_f64) {

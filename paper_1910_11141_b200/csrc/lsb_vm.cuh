@@ -345,7 +345,16 @@ __device__ inline void compute_op(const VMArgs& a, const ROp& op, const uint64_t
 __device__ inline void write_output(const VMArgs& a, const Lane& ln, long long chain) {
   const uint64_t* src = ln.top(a.output_row, a.output_sp, a.out_width);
   uint64_t* dst = a.output + (size_t)chain * a.out_width;
-  for (int i = 0; i < a.out_width; ++i) dst[i] = src[(size_t)i * ln.L];
+  const int w = a.out_width;
+  int i = 0;
+  for (; i + 16 <= w; i += 16) {  // 16 loads in flight before the stores
+    uint64_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = src[(size_t)(i + j) * ln.L];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) dst[i + j] = v[j];
+  }
+  for (; i < w; ++i) dst[i] = src[(size_t)i * ln.L];
 }
 
 __device__ inline void init_lane(const VMArgs& a, const Lane& ln, long long chain) {
@@ -383,44 +392,91 @@ __device__ __forceinline__ const double* staged_B(const VMArgs& a, int t) {
   return (a.stage_doubles > 0 && t == a.stage_target) ? lsb_dyn_smem : nullptr;
 }
 
-template <bool SB>
+// Shared-memory row stride (doubles) of a staged 8-chain tile: DMMA A-fragment
+// loads (8 rows x 4 cols, 64-bit) are bank-conflict free.
+__host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8 * 8; return s + ((12 - s % 16) + 16) % 16; }
+
+// Stage x[0..d) of m-tile mt's 8 chains (rows; zero padded to SQ columns and for
+// missing chains) into Xs[8][SQ]. Thread (k % 4, row r) reads x[k][lane_r], so each
+// load instruction covers 4 workspace rows x 8 lanes (64-byte runs when the lanes
+// are contiguous), 8 loads in flight per thread.
+__device__ __forceinline__ void stage_mtile(double* Xs, int SQ, const uint64_t* myx, unsigned mask, int n,
+                                            int mt, int d) {
+  const int lane = threadIdx.x & 31;
+  const int r = lane & 7, kq = lane >> 3;
+  const int lr = mtile_lane(mask, n, mt, r);
+  const uint64_t* xg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myx, lr < 0 ? 0 : lr);
+  constexpr int kBatch = 8;
+  for (int k0 = 0; k0 < SQ; k0 += 4 * kBatch) {
+    double v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int k = k0 + 4 * i + kq;
+      v[i] = (lr >= 0 && k < d) ? as_f64(xg[(size_t)k * 32]) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int k = k0 + 4 * i + kq;
+      if (k < SQ) Xs[r * SQ + k] = v[i];
+    }
+  }
+}
+
+template <bool SB, bool SX>
 __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bool part, const uint64_t* xp,
-                                       uint64_t* dst, bool want_logpdf);
+                                       uint64_t* dst, bool want_logpdf, double* Xs);
 
 // grad, or fast logpdf, of a gaussian target for every participating lane of the
 // warp (lane-minor storage, stride 32). xp/dst: this lane's input and output.
-// Bs: the staged B fragments (staged_B) or nullptr.
+// Bs: the staged B fragments (staged_B) or nullptr. sm/sm_doubles: the warp's
+// shared-memory scratch; when it holds an 8-chain tile of x, the A operand is
+// staged there (coalesced) instead of read from the workspace per k-step.
 __device__ inline void warp_gauss(const DevTarget& tg, const double* Bs, bool part, const uint64_t* xp,
-                                  uint64_t* dst, bool want_logpdf) {
-  if (Bs) warp_gauss_impl<true>(tg, Bs, part, xp, dst, want_logpdf);
-  else warp_gauss_impl<false>(tg, tg.B1, part, xp, dst, want_logpdf);
+                                  uint64_t* dst, bool want_logpdf, double* sm, int sm_doubles) {
+  const bool sx = sm != nullptr && 8 * lf_stride_q(tg.dim) <= sm_doubles;
+  if (Bs) {
+    if (sx) warp_gauss_impl<true, true>(tg, Bs, part, xp, dst, want_logpdf, sm);
+    else warp_gauss_impl<true, false>(tg, Bs, part, xp, dst, want_logpdf, nullptr);
+  } else {
+    if (sx) warp_gauss_impl<false, true>(tg, tg.B1, part, xp, dst, want_logpdf, sm);
+    else warp_gauss_impl<false, false>(tg, tg.B1, part, xp, dst, want_logpdf, nullptr);
+  }
 }
 
-template <bool SB>
+template <bool SB, bool SX>
 __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bool part, const uint64_t* xp,
-                                       uint64_t* dst, bool want_logpdf) {
-  const int lane = threadIdx.x & 31;
+                                       uint64_t* dst, bool want_logpdf, double* Xs) {
+  const int lane = threadIdx.x & 31, g = lane >> 2;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n = __popc(mask);
   const int d = tg.dim;
+  const int SQ = lf_stride_q(d);
   for (int mt = 0; mt * 8 < n; ++mt) {
-    const int src = mtile_lane(mask, n, mt, lane >> 2);
+    const int src = mtile_lane(mask, n, mt, g);
     const uint64_t* xg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)xp, src < 0 ? 0 : src);
     uint64_t* dg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)dst, src < 0 ? 0 : src);
-    auto a_at = [&](int k) -> double { return (src >= 0 && k < d) ? as_f64(xg[(size_t)k * 32]) : 0.0; };
+    if constexpr (SX) {
+      __syncwarp();
+      stage_mtile(Xs, SQ, xp, mask, n, mt, d);
+      __syncwarp();
+    }
+    auto x_at = [&](int k) -> double {
+      if constexpr (SX) return Xs[g * SQ + k];
+      else return (src >= 0 && k < d) ? as_f64(xg[(size_t)k * 32]) : 0.0;
+    };
     double quad = 0.0;
     for (int nt0 = 0; nt0 < tg.NT1; nt0 += LSB_NT_CHUNK) {
       const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
       LSB_NT_DISPATCH(ntc, {
         double acc[NTC][2];
-        lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, a_at);
+        lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, x_at);
         _Pragma("unroll")
         for (int j = 0; j < NTC; ++j) {
           _Pragma("unroll")
           for (int e = 0; e < 2; ++e) {
             const int col = 8 * (nt0 + j) + 2 * (lane & 3) + e;
             if (src >= 0 && col < d) {
-              if (want_logpdf) quad = fma(as_f64(xg[(size_t)col * 32]), acc[j][e], quad);
+              if (want_logpdf) quad = fma(x_at(col), acc[j][e], quad);
               else dg[(size_t)col * 32] = f64_bits(-acc[j][e]);
             }
           }
@@ -433,6 +489,7 @@ __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bo
       if (src >= 0 && (lane & 3) == 0) dg[0] = f64_bits(tg.norm - 0.5 * quad);
     }
   }
+  if constexpr (SX) __syncwarp();
 }
 
 __device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
@@ -444,7 +501,6 @@ __device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
 // Shared-memory row strides (doubles) of the superblock tiles: DMMA A-fragment
 // loads (8 rows x 4 cols, 64-bit) and C-fragment epilogues (8 rows x 2 cols,
 // 128-bit) are bank-conflict free.
-__host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8 * 8; return s + ((12 - s % 16) + 16) % 16; }
 __host__ __device__ __forceinline__ int lf_stride_p(int d) { int s = (d + 7) / 8 * 8; return s + ((8 - s % 16) + 16) % 16; }
 // d <= 128 uses the register-momentum superblock (only q staged in shared memory)
 constexpr int kLfRegMaxTiles = 16;
@@ -477,6 +533,18 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
 // registers in the DMMA C-fragment layout, q in shared memory (A-fragment source).
 // Half the shared-memory footprint of the tile version, which leaves room for the
 // CTA-wide staged copy of the precision matrix's B fragments (Bf, SB = true).
+// Dev-only phase clock of the superblock (-DLSB_SB_PROFILE=1; tools/sb_profile.py):
+// [0] q staging, [1] p load, [2] kicks (DMMA), [3] drifts, [4] write-back, [5] calls
+#if LSB_SB_PROFILE
+__device__ unsigned long long lsb_sb_prof[8];
+#define LSB_SB_T(v) const long long v = clock64()
+#define LSB_SB_ADD(i, t0, t1) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&lsb_sb_prof[i], (unsigned long long)((t1) - (t0)))
+#else
+#define LSB_SB_T(v)
+#define LSB_SB_ADD(i, t0, t1)
+#endif
+
 template <int NT, bool SB>
 __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                  long long chain, const double* Bf) {
@@ -505,11 +573,10 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
     lane_trace_put(a, chain, head + 2);
   }
   for (int mt = 0; mt * 8 < n; ++mt) {
-    for (int r = 0; r < 8; ++r) {  // stage q of the m-tile's 8 chains (zero rows pad)
-      const int lr = mtile_lane(mask, n, mt, r);
-      const uint64_t* qg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, lr < 0 ? 0 : lr);
-      for (int k = lane; k < SQ; k += 32) Qs[r * SQ + k] = (lr >= 0 && k < d) ? as_f64(qg[(size_t)k * 32]) : 0.0;
-    }
+    LSB_SB_T(t_a);
+    stage_mtile(Qs, SQ, myq, mask, n, mt, d);  // q of the m-tile's 8 chains
+    LSB_SB_T(t_b);
+    LSB_SB_ADD(0, t_a, t_b);
     const int src = mtile_lane(mask, n, mt, g);
     const int sl = src < 0 ? 0 : src;
     const uint64_t* pg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, sl);
@@ -526,14 +593,22 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
         p[nt][e] = (src >= 0 && col < d) ? as_f64(pg[(size_t)col * 32]) : 0.0;
       }
     __syncwarp();
+#if LSB_SB_PROFILE
+    if (p[0][0] == 123.456) p[0][1] = 0.0;  // force the p loads to complete here
+#endif
+    LSB_SB_T(t_c);
+    LSB_SB_ADD(1, t_b, t_c);
     for (int it = 0; it < steps; ++it) {
       for (int hs = 0; hs < 2; ++hs) {
         const bool last = (it == steps - 1) && hs == 1;
+        LSB_SB_T(t_k0);
         lf_kick<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
         if constexpr (NT > 4) lf_kick<NT, 4, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
         if constexpr (NT > 8) lf_kick<NT, 8, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
         if constexpr (NT > 12) lf_kick<NT, 12, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
         __syncwarp();
+        LSB_SB_T(t_k1);
+        LSB_SB_ADD(2, t_k0, t_k1);
         if (hs == 0) {  // drift: q = e p + q on this thread's (row, columns)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
@@ -543,9 +618,12 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
               if (col < d) Qs[g * SQ + col] = __dadd_rn(__dmul_rn(eg, p[nt][e]), Qs[g * SQ + col]);
             }
           __syncwarp();
+          LSB_SB_T(t_k2);
+          LSB_SB_ADD(3, t_k1, t_k2);
         }
       }
     }
+    LSB_SB_T(t_w0);
     // write back q, p and _ret = vcat(q, p): each thread its (row, columns)
     uint64_t* qo = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myq, sl);
     uint64_t* po = (uint64_t*)__shfl_sync(kFull, (unsigned long long)myp, sl);
@@ -566,7 +644,12 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
         }
     }
     __syncwarp();
+    LSB_SB_T(t_w1);
+    LSB_SB_ADD(4, t_w0, t_w1);
   }
+#if LSB_SB_PROFILE
+  if (lane == 0) atomicAdd(&lsb_sb_prof[5], 1ull);
+#endif
 }
 
 // Fused leapfrog superblock: the whole `leapfrog(q, p, e)` function of the
@@ -582,6 +665,16 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
 template <bool SB>
 __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                    long long chain, const double* Bf);
+
+// One out-of-line register-momentum superblock for a target with NT n-tiles
+// (program-specialised builds call this directly: one compact body in the i-cache).
+template <int NT>
+__device__ __noinline__ void warp_leapfrog_nt(const VMArgs& a, const Lane& ln, const ROp& op, bool part,
+                                              double* sm, long long chain) {
+  const double* Bs = staged_B(a, op.imm0);
+  if (Bs) warp_leapfrog_rp<NT, true>(a, ln, op, part, sm, chain, Bs);
+  else warp_leapfrog_rp<NT, false>(a, ln, op, part, sm, chain, a.targets[op.imm0].B1);
+}
 
 __device__ inline void warp_leapfrog(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                      long long chain) {
@@ -752,10 +845,10 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
       if (WARP) {
         __syncwarp();
         warp_gauss(a.targets[op.imm0], staged_B(a, op.imm0), part, part ? ln.in(op, 0) : nullptr, dst,
-                   op.opcode == LS_OP_LOGPDF);
+                   op.opcode == LS_OP_LOGPDF, lf_smem, a.lf_smem_per_warp);
         __syncwarp();
       }
-    } else if (part) {
+    } else if (part && op.opcode != LS_OP_ALLOC) {  // alloc: the slot is reserved, not written
       compute_op(a, op, op.nin > 0 ? ln.in(op, 0) : nullptr, op.nin > 1 ? ln.in(op, 1) : nullptr,
                  op.nin > 2 ? ln.in(op, 2) : nullptr, dst, ln.L);
     }

@@ -137,6 +137,114 @@ def demote_unpushed(flat: ir.FlatProgram, classes: dict[str, str]) -> tuple:
     return flat, {v: ("register" if v in demoted else c) for v, c in classes.items()}
 
 
+def dead_saves(flat: ir.FlatProgram, classes: dict[str, str], labels) -> set[tuple[int, int]]:
+    """Caller saves `push v = id v` whose copied value is never observed.
+
+    A save gives the callee a fresh top slot for `v` holding a copy of the
+    caller's value, and the matching pop re-exposes the caller's slot, which
+    nothing above it can touch. When no activation of v's function reads `v`
+    before writing it (a must-defined analysis over that function's blocks,
+    parameters defined by the call block, a call that does not save `v` and
+    may re-enter the function clobbering it) and the call block itself does
+    not read `v` after the push, the copy is unobservable: the push only has
+    to allocate the slot (device opcode `alloc`). Returns (block, op) positions.
+    """
+    fn_of = [lbl.split(".", 1)[0] for lbl in labels]
+    n = len(flat.blocks)
+    stacked = {v for v, c in classes.items() if c == "stacked"}
+    vfn = {v: v.split(".", 1)[0] for v in stacked}
+    calls: dict[str, set[str]] = {}
+    callers: dict[int, list[int]] = {}
+    for bi, b in enumerate(flat.blocks):
+        if isinstance(b.terminator, ir.PushJump):
+            calls.setdefault(fn_of[bi], set()).add(fn_of[b.terminator.jump_to])
+            callers.setdefault(b.terminator.jump_to, []).append(bi)
+
+    def reaches(g: str, f: str) -> bool:
+        seen, todo = set(), [g]
+        while todo:
+            h = todo.pop()
+            if h == f:
+                return True
+            if h not in seen:
+                seen.add(h)
+                todo.extend(calls.get(h, ()))
+        return False
+
+    def pushed_in(b: int) -> set[str]:
+        return {op.output for op in flat.blocks[b].ops if isinstance(op, ir.Push)}
+
+    exposed: set[str] = set()
+    for f in set(fn_of):
+        tracked = {v for v in stacked if vfn[v] == f}
+        if not tracked:
+            continue
+        entries = [e for e in callers if fn_of[e] == f]
+        if flat.entry < n and fn_of[flat.entry] == f and flat.entry not in entries:
+            entries.append(flat.entry)
+        state: dict[int, set[str]] = {}
+        work = []
+        for e in entries:
+            if e == flat.entry and not callers.get(e):
+                d = tracked & set(flat.inputs)
+            else:  # parameters: written by every call block after its saves
+                d = None
+                for c in callers.get(e, ()):
+                    w = {op.output for op in flat.blocks[c].ops
+                         if isinstance(op, ir.Update) and op.output in tracked}
+                    d = w if d is None else d & w
+                d = d or set()
+            state[e] = d if e not in state else state[e] & d
+            work.append(e)
+        while work:
+            b = work.pop()
+            blk = flat.blocks[b]
+            d = set(state[b])
+            ret_of = [c for c in range(n) if isinstance(flat.blocks[c].terminator, ir.PushJump)
+                      and flat.blocks[c].terminator.return_to == b]
+            saved_before = set.intersection(*(pushed_in(c) for c in ret_of)) if ret_of else set()
+            for op in blk.ops:
+                if isinstance(op, ir.Pop):
+                    if op.var in tracked and op.var not in saved_before:
+                        d.discard(op.var)
+                    continue
+                exposed.update(v for v in op.inputs if v in tracked and v not in d)
+                if op.output in tracked:
+                    d.add(op.output)
+            t = blk.terminator
+            succ: list[tuple[int, set[str]]] = []
+            if isinstance(t, ir.FlatBranch):
+                if t.cond in tracked and t.cond not in d:
+                    exposed.add(t.cond)
+                succ = [(t.true_target, d), (t.false_target, d)]
+            elif isinstance(t, ir.FlatJump):
+                succ = [(t.target, d)]
+            elif isinstance(t, ir.PushJump):
+                nd = d if not reaches(fn_of[t.jump_to], f) else d & pushed_in(b)
+                succ = [(t.return_to, nd)]
+            for s, sd in succ:
+                if not (0 <= s < n) or fn_of[s] != f:
+                    continue
+                new = set(sd) if s not in state else state[s] & sd
+                if s not in state or new != state[s]:
+                    state[s] = new
+                    work.append(s)
+    out: set[tuple[int, int]] = set()
+    for bi, blk in enumerate(flat.blocks):
+        if not isinstance(blk.terminator, ir.PushJump):
+            continue
+        for oi, op in enumerate(blk.ops):
+            if not (isinstance(op, ir.Push) and op.prim.name == "id" and op.inputs == (op.output,)):
+                continue
+            v = op.output
+            if v not in stacked or v in exposed:
+                continue
+            if any(not isinstance(o, ir.Pop) and v in o.inputs for o in blk.ops[oi + 1:]):
+                continue
+            out.add((bi, oi))
+    return out
+
+
 def _op_liveness(flat: ir.FlatProgram):
     """live-after sets per (block, op index) of the flat program (Pop reads and writes)."""
     from .compiler import _flat_live_in
@@ -596,11 +704,13 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     leapfrog function entry with one fused LS_OP_LEAPFROG op + return.
     """
     flat, classes = compiled.flat, dict(compiled.classes)
+    allocs: set[tuple[int, int]] = set()
     if optimize:
         flat, classes = demote_nonreentrant(flat, classes, compiled.labels)
         flat, classes = demote_unpushed(flat, classes)
         flat = fuse_copies(flat, classes)
         flat = coalesce_copies(flat, classes)
+        allocs = dead_saves(flat, classes, compiled.labels)
     fused = {}
     if optimize and superblocks:
         for m in match_leapfrog(flat, classes, grad_names()):
@@ -637,10 +747,16 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             conds.append(None)
             block_ops.append(ops)
             continue
-        for op in blk.ops:
+        for oi, op in enumerate(blk.ops):
             if isinstance(op, ir.Pop):
                 ops.append(dict(opcode=0, action=ACTION_POP, out=op.var, ins=[], kind=0, width=1,
                                 imm0=0, imm1=0, imm2=0, bits=0, prim="$pop"))
+                continue
+            if (bi, oi) in allocs:
+                vt = vtype(op.output)
+                ops.append(dict(opcode=OPCODES["alloc"], action=ACTION_PUSH, out=op.output, ins=[],
+                                kind=KIND_CODE[vt.kind], width=vt.words, imm0=0, imm1=0, imm2=0, bits=0,
+                                prim="$alloc"))
                 continue
             k = resolve_kernel(op.prim.name)
             if k.device is None:

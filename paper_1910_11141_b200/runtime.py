@@ -107,6 +107,7 @@ OPCODES = {
     "rng_uniform": 31,
     "logpdf": 32, "grad": 33,
     "leapfrog": 64,  # fused superblock (lowering.match_leapfrog), never a source primitive
+    "alloc": 65,     # push of an unobserved save (lowering.dead_saves), never a source primitive
 }
 
 

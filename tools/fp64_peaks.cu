@@ -35,6 +35,41 @@ __global__ void dmma_kernel(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// latency / issue-rate probe: `warps` warps of one CTA, each with ILP independent
+// accumulator chains; reports SM cycles per DMMA per warp
+template <int ILP>
+__global__ void dmma_lat_kernel(double* out, long long* cyc, int iters) {
+  double a = threadIdx.x * 1e-3, b = 0.5;
+  double c[ILP][2];
+  for (int t = 0; t < ILP; ++t) { c[t][0] = 0; c[t][1] = 0; }
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < ILP; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int t = 0; t < ILP; ++t) s += c[t][0] + c[t][1];
+  const long long t1 = clock64();
+  out[threadIdx.x] = s;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+
+template <int ILP>
+void lat_probe(double* out, long long* dcyc) {
+  for (int warps : {1, 4, 8, 16}) {
+    const int iters = 4000;
+    dmma_lat_kernel<ILP><<<1, 32 * warps>>>(out, dcyc, 10);
+    dmma_lat_kernel<ILP><<<1, 32 * warps>>>(out, dcyc, iters);
+    long long cyc = 0;
+    cudaMemcpy(&cyc, dcyc, sizeof(cyc), cudaMemcpyDeviceToHost);
+    printf("{\"probe\": \"dmma_latency\", \"ilp\": %d, \"warps_per_sm\": %d, \"cycles_per_dmma_per_warp\": %.2f}\n",
+           ILP, warps, (double)cyc / ((double)iters * ILP));
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -67,6 +102,12 @@ int main() {
     const double flops = 2.0 * 8 * 8 * 4 * 8 * (double)iters * blocks * (threads / 32);
     printf("{\"pipe\": \"dmma_m8n8k4\", \"threads\": %d, \"tflops\": %.2f}\n", threads, flops / ms / 1e9);
   }
+  long long* dcyc;
+  cudaMalloc(&dcyc, sizeof(long long));
+  lat_probe<1>(out, dcyc);
+  lat_probe<2>(out, dcyc);
+  lat_probe<4>(out, dcyc);
+  lat_probe<8>(out, dcyc);
   cudaError_t e = cudaGetLastError();
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(e));
   return e != cudaSuccess;
