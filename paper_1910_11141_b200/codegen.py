@@ -49,7 +49,11 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # loads in flight per thread in the generated vector loops
        "ewu": int(os.environ.get("LSB_CG_EWU", "16")),
        # dev-only superblock phase clocks (tools/sb_profile.py)
-       "sbprof": int(os.environ.get("LSB_CG_SBPROF", "0"))}
+       "sbprof": int(os.environ.get("LSB_CG_SBPROF", "0")),
+       # n-tiles per superblock kick pass
+       "lfkc": int(os.environ.get("LSB_CG_LFKC", "2")),
+       # shared out-of-line vector helpers instead of a loop per call site
+       "ool": int(os.environ.get("LSB_CG_OOL", "0"))}
 
 
 def _u64(bits: int) -> str:
@@ -220,7 +224,8 @@ class _Gen:
         elif name == "rng_uniform":
             kf = str(self.vars[ins[0]]["kind"] == F64).lower()
             cf = str(self.vars[ins[1]]["kind"] == F64).lower()
-            expr = f"f64_bits(lsb::rng_uniform(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf})))"
+            expr = (f"ool_rng(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf}))" if OPT["ool"] else
+                    f"f64_bits(lsb::rng_uniform(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf})))")
         elif name == "dot":
             expr = f"f64_bits(dot<{W(0)}>({P(0)}, {P(1)}))"
         elif name == "logpdf":
@@ -266,8 +271,12 @@ class _Gen:
                         "div": "i64_div(xs_[i * S], ys_[i * S])",
                         "min": "i_min(xs_[i * S], ys_[i * S], true)",
                         "max": "i_min(xs_[i * S], ys_[i * S], false)"}[name]
-            lines.append(f"  {{ const uint64_t* xs_ = {xs}; const uint64_t* ys_ = {ys};")
-            lines.append(f"    ew<{width}>(d_, [&](int i) {{ return {body}; }}); }}")
+            code = {"add": 0, "sub": 1, "mul": 2, "div": 3}.get(name)
+            if OPT["ool"] and fk and code is not None:
+                lines.append(f"  binop_f64_n(d_, {xs}, {ys}, {width}, {code});")
+            else:
+                lines.append(f"  {{ const uint64_t* xs_ = {xs}; const uint64_t* ys_ = {ys};")
+                lines.append(f"    ew<{width}>(d_, [&](int i) {{ return {body}; }}); }}")
         elif name in ("neg", "abs", "sqrt", "exp", "log", "sin", "cos", "floor"):
             if fk:
                 fn = {"neg": None, "abs": "fabs", "sqrt": "__dsqrt_rn", "floor": "floor"}.get(name, f"ool_{name}")
@@ -451,6 +460,7 @@ class _Gen:
         out = ["// generated by paper_1910_11141_b200/codegen.py — do not edit",
                f"// options: {sorted(OPT.items())}", "#pragma once",
                f"#define LSB_GEN_STAGED {int(OPT['staged'])}",
+               f"#define LSB_GEN_OOL {int(OPT['ool'])}",
                '#include "lsb_gen_rt.cuh"', "namespace lsbgen {",
                "__device__ __forceinline__ bool finish_block(const VMArgs& a, const Lane& ln, int term, int ta, int tb,",
                "                                             bool cond, int pos, StepFault& f) {",
@@ -503,7 +513,7 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
            f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}",
-           f"-DLSB_SB_PROFILE={OPT['sbprof']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
+           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_LF_KC={OPT['lfkc']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=str(_build.ROOT))

@@ -92,6 +92,37 @@ __device__ __forceinline__ void mtile_gemm(double (&acc)[NTC][2], const double* 
 #endif
 }
 
+// mtile_gemm with the A and B fragments of step k+1 loaded (into distinct
+// registers) while step k's DMMAs run: the LDS latency hides behind the MMAs.
+// For operands in shared memory (A tile and, with SB, the staged B fragments).
+template <int NTC, bool SB, class ALoad>
+__device__ __forceinline__ void mtile_gemm_pf(double (&acc)[NTC][2], const double* __restrict__ Bf,
+                                              int KS, int NT, int nt0, const ALoad& a_at) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) acc[j][0] = acc[j][1] = 0.0;
+  const double* bp = Bf + (size_t)nt0 * 32 + lane;
+  const int kstride = NT * 32;
+  double a = a_at(lane & 3), b[NTC];
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) b[j] = ld_b<SB>(bp + j * 32);
+#pragma unroll 1
+  for (int ks = 0; ks + 1 < KS; ++ks) {
+    bp += kstride;
+    const double an = a_at(4 * (ks + 1) + (lane & 3));
+    double bn[NTC];
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) bn[j] = ld_b<SB>(bp + j * 32);
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) dmma(acc[j], a, b[j]);
+    a = an;
+#pragma unroll
+    for (int j = 0; j < NTC; ++j) b[j] = bn[j];
+  }
+#pragma unroll
+  for (int j = 0; j < NTC; ++j) dmma(acc[j], a, b[j]);
+}
+
 // n-tiles per accumulator pass: 8 tiles = 16 fp64 accumulators per lane (32 registers)
 #define LSB_NT_CHUNK 8
 

@@ -40,9 +40,63 @@ __device__ __forceinline__ void ew(uint64_t* dst, const F& f) {
   for (int i = full; i < W; ++i) dst[i * S] = f(i);
 }
 
+#ifndef LSB_GEN_OOL
+#define LSB_GEN_OOL 0
+#endif
+
+// Runtime-width form of ew for the shared out-of-line helpers below: kEw loads in
+// flight per batch, the tail as one predicated batch.
+template <class F>
+__device__ __forceinline__ void ew_n(uint64_t* dst, int w, const F& f) {
+#pragma unroll 1
+  for (int i = 0; i < w; i += kEw) {
+    uint64_t v[kEw];
+    if (i + kEw <= w) {
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) v[j] = f(i + j);
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) dst[(i + j) * S] = v[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < kEw; ++j)
+        if (i + j < w) v[j] = f(i + j);
+#pragma unroll
+      for (int j = 0; j < kEw; ++j)
+        if (i + j < w) dst[(i + j) * S] = v[j];
+    }
+  }
+}
+
+// Out-of-line vector helpers (LSB_GEN_OOL): every block calls one shared body
+// instead of inlining a loop per call site, which keeps the generated program's
+// instruction footprint small enough for the SM instruction caches.
+__device__ __noinline__ void copy_n(uint64_t* dst, const uint64_t* src, int w) {
+  if (dst != src) ew_n(dst, w, [&](int i) { return src[i * S]; });
+}
+__device__ __noinline__ void fill_n(uint64_t* dst, uint64_t v, int w) {
+  ew_n(dst, w, [&](int) { return v; });
+}
+__device__ __noinline__ void axpy_n(uint64_t* dst, double s, const uint64_t* x, const uint64_t* y, int w) {
+  ew_n(dst, w, [&](int i) { return f64_bits(__dadd_rn(__dmul_rn(s, as_f64(x[i * S])), as_f64(y[i * S]))); });
+}
+// f64 add / sub / mul / div (op 0..3), IEEE round-to-nearest like compute_op
+__device__ __noinline__ void binop_f64_n(uint64_t* dst, const uint64_t* x, const uint64_t* y, int w, int op) {
+  switch (op) {
+    case 0: ew_n(dst, w, [&](int i) { return f64_bits(__dadd_rn(as_f64(x[i * S]), as_f64(y[i * S]))); }); break;
+    case 1: ew_n(dst, w, [&](int i) { return f64_bits(__dsub_rn(as_f64(x[i * S]), as_f64(y[i * S]))); }); break;
+    case 2: ew_n(dst, w, [&](int i) { return f64_bits(__dmul_rn(as_f64(x[i * S]), as_f64(y[i * S]))); }); break;
+    default: ew_n(dst, w, [&](int i) { return f64_bits(__ddiv_rn(as_f64(x[i * S]), as_f64(y[i * S]))); }); break;
+  }
+}
+__device__ __noinline__ uint64_t ool_rng(int64_t key, int64_t c) { return f64_bits(lsb::rng_uniform(key, c)); }
+
 template <int W>
 __device__ __forceinline__ void copy(uint64_t* dst, const uint64_t* src) {
+#if LSB_GEN_OOL
+  copy_n(dst, src, W);
+#else
   if (dst != src) ew<W>(dst, [&](int i) { return src[i * S]; });
+#endif
 }
 
 // Copy between rows the generator proved disjoint: with __restrict__ and a static
@@ -85,24 +139,64 @@ __device__ __noinline__ double ool_cos(double x) { return cos(x); }
 
 template <int W>
 __device__ __forceinline__ void fill(uint64_t* dst, uint64_t v) {
+#if LSB_GEN_OOL
+  if constexpr (W > 4) { fill_n(dst, v, W); return; }
+#endif
   ew<W>(dst, [&](int) { return v; });
 }
 
 template <int W>
 __device__ __forceinline__ void axpy(uint64_t* dst, double s, const uint64_t* x, const uint64_t* y) {
+#if LSB_GEN_OOL
+  axpy_n(dst, s, x, y, W);
+#else
   ew<W>(dst, [&](int i) { return f64_bits(__dadd_rn(__dmul_rn(s, as_f64(x[i * S])), as_f64(y[i * S]))); });
+#endif
 }
 
 template <int W>
 __device__ __forceinline__ void select(uint64_t* dst, bool c, const uint64_t* x, const uint64_t* y) {
   const uint64_t* src = c ? x : y;
+#if LSB_GEN_OOL
+  copy_n(dst, src, W);
+#else
   if (src != dst) ew<W>(dst, [&](int i) { return src[i * S]; });
+#endif
 }
 
 // (x*y).sum(): numpy's pairwise order (lsb_ops.cuh pairwise). For a static
 // W <= 128 the whole sum is unrolled so the loads can all be issued early.
+// Shared out-of-line (x*y).sum() for 8 <= w <= 128 in numpy's pairwise order,
+// 16 products loaded per batch.
+__device__ __noinline__ double dot_n(const uint64_t* x, const uint64_t* y, int w) {
+  auto p = [&](int i) { return __dmul_rn(as_f64(x[i * S]), as_f64(y[i * S])); };
+  const int stop = w - w % 8;
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = p(j);
+#pragma unroll 1
+  for (int i = 8; i < stop; i += 16) {
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = (i + j < stop) ? p(i + j) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[j]);
+    if (i + 8 < stop) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[8 + j]);
+    }
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (int i = stop; i < w; ++i) res = __dadd_rn(res, p(i));
+  return __dadd_rn(0.0, res);
+}
+
 template <int W>
 __device__ __forceinline__ double dot(const uint64_t* x, const uint64_t* y) {
+#if LSB_GEN_OOL
+  if constexpr (W >= 8 && W <= 128) return dot_n(x, y, W);
+#endif
   if constexpr (W < 8 || W > 128) {
     return lsb::dot_lane(x, y, W, S);
   } else {

@@ -19,6 +19,10 @@
 #include "lsb_dmma.cuh"
 #include "lsb_ops.cuh"
 
+#ifndef LSB_LF_KC
+#define LSB_LF_KC 2  // n-tiles per superblock kick pass
+#endif
+
 namespace lsbvm {
 
 using lsb::as_f64;
@@ -513,10 +517,11 @@ __host__ __device__ __forceinline__ int lf_smem_doubles(int d) {
 template <int NT, int C0, bool SB>
 __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
                                         const double* Bf, double half, bool last, uint64_t* gg, int d) {
-  constexpr int NTC = (NT - C0) < 4 ? (NT - C0) : 4;  // 4 n-tiles per pass: p + acc fit in registers
+  // LSB_LF_KC n-tiles per pass: p (in registers) + acc + prefetched fragments fit
+  constexpr int NTC = (NT - C0) < LSB_LF_KC ? (NT - C0) : LSB_LF_KC;
   const int lane = threadIdx.x & 31, g = lane >> 2;
   double acc[NTC][2];
-  lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, C0, [&](int k) -> double { return Qs[g * SQ + k]; });
+  lsb::mtile_gemm_pf<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, C0, [&](int k) -> double { return Qs[g * SQ + k]; });
 #pragma unroll
   for (int j = 0; j < NTC; ++j) {
 #pragma unroll
@@ -527,6 +532,14 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
       if (last && gg != nullptr && col < d) gg[(size_t)col * 32] = f64_bits(gv);
     }
   }
+}
+
+// All passes of one kick: n-tiles C0, C0 + LSB_LF_KC, ... < NT.
+template <int NT, int C0, bool SB>
+__device__ __forceinline__ void lf_kicks(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
+                                         const double* Bf, double half, bool last, uint64_t* gg, int d) {
+  lf_kick<NT, C0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+  if constexpr (C0 + LSB_LF_KC < NT) lf_kicks<NT, C0 + LSB_LF_KC, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
 }
 
 // Register-momentum variant of the fused leapfrog superblock (d <= 128): p lives in
@@ -602,10 +615,7 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
       for (int hs = 0; hs < 2; ++hs) {
         const bool last = (it == steps - 1) && hs == 1;
         LSB_SB_T(t_k0);
-        lf_kick<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
-        if constexpr (NT > 4) lf_kick<NT, 4, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
-        if constexpr (NT > 8) lf_kick<NT, 8, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
-        if constexpr (NT > 12) lf_kick<NT, 12, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
         __syncwarp();
         LSB_SB_T(t_k1);
         LSB_SB_ADD(2, t_k0, t_k1);
