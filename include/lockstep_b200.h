@@ -15,7 +15,7 @@
  *   ls_run
  *       <- pc_vm.run_vm / pc_vm.step (pc_vm.py:304-349): batched block steps
  *          until every lane halts, StepLimitExceeded, stack faults
- *   ls_read_output
+ *   ls_read_output (+ ls_host_alloc / ls_host_free for page-locked destinations)
  *       <- Machine.output_value (pc_vm.py:136-137): a copy of the output var
  *   ls_trace_fetch / ls_block_totals
  *       <- ScheduleTrace.record (metrics.py:36-37), one record per step
@@ -228,6 +228,11 @@ int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count);
 int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap);
 int ls_machine_sync(ls_machine* m);
 int ls_machine_destroy(ls_machine* m);
+
+/* page-locked host buffers: ls_read_output into one is a direct DMA (the host-side
+   output pool of the Python binding, _native.HostPool) */
+int ls_host_alloc(int64_t bytes, void** host);
+int ls_host_free(void* host);
 
 /* runtime.rng_uniform over n lanes (keys/counters as int64 after numpy's astype) */
 int ls_rng_uniform(const int64_t* key, const int64_t* counter, int64_t n, double* out);

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import re
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -50,6 +51,8 @@ class Status(C.Structure):
 
 _SIGS = {
     "ls_abi_version": ([], C.c_int),
+    "ls_host_alloc": ([C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
+    "ls_host_free": ([C.c_void_p], C.c_int),
     "ls_last_error": ([], C.c_char_p),
     "ls_device_count": ([C.POINTER(C.c_int32)], C.c_int),
     "ls_program_create": ([C.POINTER(ProgramDesc), C.POINTER(C.c_void_p)], C.c_int),
@@ -160,6 +163,68 @@ class Program:
             self.handle = None
 
 
+class _PinnedBuf:
+    """One page-locked host allocation (ls_host_alloc); freed when unreferenced."""
+
+    __slots__ = ("lib", "ptr", "nbytes")
+
+    def __init__(self, lib, nbytes: int):
+        p = C.c_void_p()
+        _check(lib.ls_host_alloc(nbytes, C.byref(p)), lib)
+        self.lib, self.ptr, self.nbytes = lib, p.value, nbytes
+
+    def __del__(self):
+        try:
+            self.lib.ls_host_free(C.c_void_p(self.ptr))
+        except Exception:  # interpreter teardown
+            pass
+
+
+class _HostView:
+    """numpy base object that keeps a pinned buffer alive while any view exists."""
+
+    def __init__(self, buf: _PinnedBuf, shape: tuple[int, ...]):
+        self.buf = buf
+        self.__array_interface__ = {"data": (buf.ptr, False), "shape": shape, "typestr": "<u8",
+                                    "version": 3}
+
+
+class HostPool:
+    """Page-locked destinations for large output reads (a caching host allocator).
+
+    ls_read_output into pinned memory is one DMA at PCIe rate, while a fresh
+    pageable array costs first-touch page faults plus the driver's staging copy.
+    A buffer is handed out again only when no array returned from it is still
+    referenced (its refcount is back to the pool's own), so results a caller
+    keeps are never overwritten; when every buffer is busy the pool grows up to
+    `cap` buffers per size, then callers fall back to ordinary numpy memory.
+    """
+
+    def __init__(self, cap: int = 3, min_bytes: int = 1 << 22):
+        self.cap, self.min_bytes = cap, min_bytes
+        self.bufs: dict[int, list[_PinnedBuf]] = {}
+
+    def array(self, lib, shape: tuple[int, ...]) -> np.ndarray | None:
+        nbytes = int(np.prod(shape)) * 8
+        if nbytes < self.min_bytes:
+            return None
+        free = self.bufs.setdefault(nbytes, [])
+        for b in free:
+            if sys.getrefcount(b) <= 3:  # the list, the loop variable, the call argument
+                return np.asarray(_HostView(b, shape))
+        if len(free) >= self.cap:
+            return None
+        try:
+            b = _PinnedBuf(lib, nbytes)
+        except DeviceError:
+            return None
+        free.append(b)
+        return np.asarray(_HostView(b, shape))
+
+
+HOST_POOL = HostPool()
+
+
 class MachineHandle:
     """Owns an `ls_machine` (device storage for one batch of lanes)."""
 
@@ -199,7 +264,10 @@ class MachineHandle:
         return st
 
     def read_output(self, width: int, dtype) -> np.ndarray:
-        out = np.empty((self.z, width), dtype=np.uint64)
+        """A fresh host array of the output (pinned from HOST_POOL when large)."""
+        out = HOST_POOL.array(self.lib, (self.z, width))
+        if out is None:
+            out = np.empty((self.z, width), dtype=np.uint64)
         self._c(self.lib.ls_read_output(self.handle, _ptr(out), out.nbytes))
         return out.view(dtype)
 

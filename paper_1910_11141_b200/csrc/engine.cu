@@ -912,6 +912,22 @@ int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
   return LS_OK;
 }
 
+int ls_host_alloc(int64_t bytes, void** host) {
+  if (!host || bytes <= 0) return fail(LS_EINVAL, "bad host allocation request");
+  *host = nullptr;
+  if (cudaHostAlloc(host, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    *host = nullptr;
+    return fail(LS_ENOMEM, "cudaHostAlloc failed");
+  }
+  return LS_OK;
+}
+
+int ls_host_free(void* host) {
+  if (host) CK(cudaFreeHost(host));
+  return LS_OK;
+}
+
 int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
   if (!m || !dev_dst) return fail(LS_EINVAL, "null machine");
   if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");

@@ -257,7 +257,8 @@ class Machine:
     def output_value(self) -> np.ndarray:
         if self.halted or not self.exact:
             vt = self._dp.types[self.flat.output]
-            return _decode(self._h.read_output(vt.words, np.uint64).reshape(self.z, vt.words), vt).copy()
+            # read_output hands back a fresh array (never aliased by the machine)
+            return _decode(self._h.read_output(vt.words, np.uint64).reshape(self.z, vt.words), vt)
         return np.array(self.value_of(self.flat.output), copy=True)
 
 

@@ -342,3 +342,23 @@ def test_warp_engine_nuts_lanes_exact(codegen, exact_logpdf):
             // (2 * cfg.leaf_steps) * 2
         assert tr.useful_invocations({t.grad}) == m.useful_grads > 0
         assert m.useful_grads == want
+
+
+def test_pinned_output_pool_never_overwrites_live_results(corpus_compiled):
+    """Large outputs come back in page-locked pool buffers (_native.HOST_POOL); a
+    buffer is reused only once every array taken from it is gone."""
+    _, _, cp = corpus_compiled["fibonacci"]
+    z = 1 << 20  # 8 MiB of output: above the pool threshold
+    a = np.arange(z, dtype=np.int64) % 11
+    b = (np.arange(z, dtype=np.int64) * 7) % 11
+    out_a, _ = L.run(cp, [a], depth=64, engine="warp")
+    keep = out_a.copy()
+    out_b, _ = L.run(cp, [b], depth=64, engine="warp")
+    assert np.array_equal(out_a, keep)  # the first result survived the second run
+    assert out_a.__array_interface__["data"][0] != out_b.__array_interface__["data"][0]
+    ptr_a = out_a.__array_interface__["data"][0]
+    del out_a, keep
+    out_c, _ = L.run(cp, [a], depth=64, engine="warp")
+    assert out_c.__array_interface__["data"][0] == ptr_a  # the released buffer is recycled
+    want = oracle_run(cp, [a[:4096]], depth=64).output
+    assert np.array_equal(out_c[:4096], want)
