@@ -92,6 +92,10 @@ enum ls_opcode {
   /* push that only allocates the new top slot: a caller save whose copy is never
      read (lowering.dead_saves); overflow-checked like any push */
   LS_OP_ALLOC = 65,
+  /* fused momentum draw: the whole draw_normals(key, c) function of NUTS-lite
+     (k Box-Muller normals from counters c+0.., then c + 2*ceil(k/2)) per lane;
+     imm0 = k, imm1 = ceil(k/2); see lowering.match_normals */
+  LS_OP_NORMALS = 66,
 };
 
 /* ---- target kinds (workloads.correlated_gaussian / logistic_regression) ------ */

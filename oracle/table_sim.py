@@ -23,7 +23,7 @@ OPN = {1: "const", 2: "id", 3: "add", 4: "sub", 5: "mul", 6: "div", 7: "min", 8:
        10: "lt", 11: "eq", 12: "and", 13: "or", 14: "not", 15: "neg", 16: "abs", 17: "sqrt",
        18: "exp", 19: "log", 20: "sin", 21: "cos", 22: "floor", 23: "select", 24: "dot",
        25: "axpy", 26: "vget", 27: "vstore", 28: "vcat", 29: "vfill", 30: "vslice", 31: "rng_uniform",
-       32: "logpdf", 33: "grad", 65: "alloc"}
+       32: "logpdf", 33: "grad", 65: "alloc", 66: "normals"}
 
 
 class Fault(Exception):
@@ -172,6 +172,20 @@ def _compute(op, vec, vars_, targets, as_i64):
             k = as_i64(xs[0][0], vars_[ins[0]]["kind"])
             c = as_i64(xs[1][0], vars_[ins[1]]["kind"])
             return O.rng_uniform(np.array([k]), np.array([c])).view(np.uint64)
+        if name == "normals":  # fused draw_normals: the reference op sequence per pair
+            key = as_i64(xs[0][0], vars_[ins[0]]["kind"])
+            c = xs[1].view(np.float64)[0]
+            k, pairs = int(op["imm0"]), int(op["imm1"])
+            out = np.zeros(k + 1, np.float64)
+            for pr in range(pairs):
+                ua, ub = (O.rng_uniform(np.array([key]), np.array([as_i64(_w(c + float(j)), 0)]))[0]
+                          for j in (2 * pr, 2 * pr + 1))
+                r = np.sqrt(0.0 - 2.0 * np.log(1.0 - ua))
+                out[2 * pr] = r * np.cos(6.283185307179586 * ub)
+                if 2 * pr + 1 < k:
+                    out[2 * pr + 1] = r * np.sin(6.283185307179586 * ub)
+            out[k] = c + float(2 * pairs)
+            return out.view(np.uint64)
         if name in ("logpdf", "grad"):
             t = targets[int(op["imm0"])]
             x = xs[0].view(np.float64)[None]

@@ -53,7 +53,13 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # n-tiles per superblock kick pass
        "lfkc": int(os.environ.get("LSB_CG_LFKC", "2")),
        # shared out-of-line vector helpers instead of a loop per call site
-       "ool": int(os.environ.get("LSB_CG_OOL", "0"))}
+       "ool": int(os.environ.get("LSB_CG_OOL", "0")),
+       # blocks with more ops than this run on the (i-cache resident) op interpreter:
+       # straight-line code for e.g. draw_normals' 1300 ops misses the i-cache on
+       # every fetch (0 = always generate)
+       "interp_min": int(os.environ.get("LSB_CG_INTERP_MIN", "0")),
+       # hoist constant-index element reads of unwritten storage to the segment start
+       "hoist": int(os.environ.get("LSB_CG_HOIST", "1"))}
 
 
 def _u64(bits: int) -> str:
@@ -238,6 +244,10 @@ class _Gen:
         lines += dst
         if name == "alloc":  # unobserved save: allocate the slot, copy nothing
             return lines + ["  (void)d_;"] + post + ["}"]
+        if name == "normals":
+            kf = str(self.vars[ins[0]]["kind"] == F64).lower()
+            return lines + [f"  normals_lane(d_, S, to_i64({S(0)}, {kf}), as_f64({S(1)}), {int(op['imm0'])}, "
+                            f"{int(op['imm1'])});"] + post + ["}"]
         if expr is not None:
             lines.append(f"  d_[0] = {expr};")
         elif name == "id":
@@ -379,9 +389,53 @@ class _Gen:
             return t.kind == 1
         return False
 
+    def hoistable_loads(self, ops, i, j, locals_) -> dict[int, str]:
+        """Scalar element reads `s = vget(v, const)` of flat storage, issued together
+        right after the last write of that storage in the segment (or at its start),
+        so their memory latencies overlap instead of alternating with the stores
+        that consume them (e.g. the 100 `chain = vstore(chain, base + k, vget(q, k))`
+        of the chain store). Returns {op index: (emit-before index, line)}."""
+        consts, defs = {}, {}
+        written: dict[int, tuple[int, int]] = {}
+        for k, op in enumerate(ops):
+            if int(op["action"]) == POP:
+                continue
+            out = int(op["out"])
+            defs[out] = defs.get(out, 0) + 1
+            if OP.get(int(op["opcode"])) == "const" and int(op["kind"]) == I64:
+                consts[out] = int(op["bits"])
+            if self.cls(out) != STACKED:
+                r0 = int(self.vars[out]["row"])
+                written[k] = (r0, r0 + max(1, int(op["width"])))
+        out_lines = {}
+        for k in range(i, j):
+            op = ops[k]
+            if OP.get(int(op["opcode"])) != "vget" or int(op["action"]) != UPDATE:
+                continue
+            out, src, idx = int(op["out"]), int(op["in"][0]), int(op["in"][1])
+            if out not in locals_ or self.cls(src) == STACKED or idx not in consts or defs.get(idx) != 1:
+                continue
+            if defs.get(out) != 1:
+                continue
+            r0 = int(self.vars[src]["row"])
+            r1 = r0 + self.w(src)
+            h = i  # just after the last write of the source rows before k in this segment
+            for w in range(i, k):
+                if w in written and written[w][0] < r1 and r0 < written[w][1]:
+                    h = w + 1
+            if h >= k:
+                continue
+            e = min(max(consts[idx], 0), self.w(src) - 1)
+            out_lines[k] = (h, f"s{out} = ln.row({r0})[{e} * S];")
+        return out_lines
+
     def block(self, b):
         blk = self.dp.blocks[b]
         ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
+        if OPT["interp_min"] and len(ops) > OPT["interp_min"]:
+            return (f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane& ln, bool active, "
+                    f"long long chain, StepFault& f, double* sm) {{\n"
+                    f"  return exec_block<true>(a, ln, {b}, active, chain, f, sm);\n}}")
         # scalar block-local temporaries -> registers
         locals_ = set()
         for op in ops:
@@ -429,8 +483,15 @@ class _Gen:
             body.append(f"  const bool ran{seg} = ok;")
             body.append("  if (ok) {")
             body += [f"    sp{r} = ln.sp_row({r});" for r in sorted(rows)]
+            hoisted = self.hoistable_loads(ops, i, j, locals_) if OPT["hoist"] else {}
+            at: dict[int, list[str]] = {}
+            for k, (h, line) in hoisted.items():
+                at.setdefault(h, []).append(line)
+            body += ["    " + s for s in at.get(i, [])]
             while i < j:
-                body += ["    " + s for s in self.op_code(i, ops[i], locals_, i + 1)]
+                if i not in hoisted:
+                    body += ["    " + s for s in self.op_code(i, ops[i], locals_, i + 1)]
+                body += ["    " + s for s in at.get(i + 1, [])]
                 i += 1
             body.append("  }")
             body.append(f"  {self.end}:;")

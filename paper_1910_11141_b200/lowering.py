@@ -454,6 +454,127 @@ def match_leapfrog(flat: ir.FlatProgram, classes: dict[str, str], grads: frozens
     return found
 
 
+def _const_f64(op) -> float | None:
+    if isinstance(op, ir.Update) and op.prim.name.startswith("const:f64:") and not op.inputs:
+        return float(op.prim.name.split(":", 2)[2])
+    return None
+
+
+def match_normals(flat: ir.FlatProgram, classes: dict[str, str], labels) -> list[dict]:
+    """Find Box-Muller momentum draws of the NUTS-lite program (reference
+    workloads.py draw_normals; our workloads._normals emits the same text).
+
+    One block ending in a return whose ops are, for pr = 0 .. P-1 (a = 2pr, b = a+1):
+        Ta = const a; Xa = add c Ta; ua = rng_uniform key Xa      (same for b -> ub)
+        r = sqrt(sub(0.0, mul(2.0, log(sub(1.0, ua)))))
+        za = mul r (cos (mul 2pi ub));  [zb = mul r (sin (mul 2pi ub))  if b < k]
+    then the left-to-right vcat of vfill:1(z0 .. z_{k-1}) and vfill:1(c + 2P) into
+    the returned register. Every intermediate is a block-local temporary.
+    """
+    two_pi = 6.283185307179586
+    found = []
+    fn_of = [lbl.split(".", 1)[0] for lbl in labels]
+    entries = {b.terminator.jump_to for b in flat.blocks if isinstance(b.terminator, ir.PushJump)}
+    for b in sorted(entries):
+        blk = flat.blocks[b]
+        if not isinstance(blk.terminator, ir.FlatReturn):
+            continue
+        ops = blk.ops
+        if any(not isinstance(o, ir.Update) for o in ops):
+            continue
+        pos = 0
+
+        def take(prim, n_in=None):
+            nonlocal pos
+            if pos >= len(ops):
+                raise ValueError
+            o = ops[pos]
+            if o.prim.name != prim or (n_in is not None and len(o.inputs) != n_in):
+                raise ValueError
+            pos += 1
+            return o
+
+        def take_const(value):
+            nonlocal pos
+            if pos >= len(ops) or _const_f64(ops[pos]) != value:
+                raise ValueError
+            pos += 1
+            return ops[pos - 1].output
+
+        try:
+            key = c = None
+            zs: list[str] = []
+            pr = 0
+            while pos < len(ops) and ops[pos].prim.name.startswith("const:f64:") and \
+                    _const_f64(ops[pos]) == float(2 * pr) and pos + 1 < len(ops) and \
+                    ops[pos + 1].prim.name == "add":
+                us = []
+                for off in (0, 1):
+                    t = take_const(float(2 * pr + off))
+                    x = take("add", 2)
+                    if c is None:
+                        c = x.inputs[0]
+                    if x.inputs != (c, t):
+                        raise ValueError
+                    u = take("rng_uniform", 2)
+                    if key is None:
+                        key = u.inputs[0]
+                    if u.inputs != (key, x.output):
+                        raise ValueError
+                    us.append(u.output)
+                ua, ub = us
+                t0, t2, t1 = take_const(0.0), take_const(2.0), take_const(1.0)
+                s1 = take("sub", 2)
+                lg = take("log", 1)
+                m2 = take("mul", 2)
+                s0 = take("sub", 2)
+                r = take("sqrt", 1)
+                if not (s1.inputs == (t1, ua) and lg.inputs == (s1.output,) and m2.inputs == (t2, lg.output)
+                        and s0.inputs == (t0, m2.output) and r.inputs == (s0.output,)):
+                    raise ValueError
+                for trig in ("cos", "sin"):
+                    if trig == "sin" and (pos >= len(ops) or _const_f64(ops[pos]) != two_pi):
+                        break
+                    tp = take_const(two_pi)
+                    mu = take("mul", 2)
+                    tr = take(trig, 1)
+                    z = take("mul", 2)
+                    if not (mu.inputs == (tp, ub) and tr.inputs == (mu.output,) and z.inputs == (r.output, tr.output)):
+                        raise ValueError
+                    zs.append(z.output)
+                pr += 1
+            k, pairs = len(zs), pr
+            if pairs == 0 or not (2 * pairs - 1 <= k <= 2 * pairs) or c is None:
+                raise ValueError
+            # pack: vfill:1 of each z, chained left to right, then vfill:1(c + 2P)
+            acc = None
+            for i, z in enumerate(zs):
+                f = take("vfill:1", 1)
+                if f.inputs != (z,):
+                    raise ValueError
+                if acc is None:
+                    acc = f.output
+                    continue
+                v = take("vcat", 2)
+                if v.inputs != (acc, f.output):
+                    raise ValueError
+                acc = v.output
+            tc = take_const(float(2 * pairs))
+            xc = take("add", 2)
+            fc = take("vfill:1", 1)
+            ret = take("vcat", 2)
+            if xc.inputs != (c, tc) or fc.inputs != (xc.output,) or ret.inputs != (acc, fc.output):
+                raise ValueError
+            if pos != len(ops) or classes.get(ret.output) != "register":
+                raise ValueError
+            if fn_of[b] != key.split(".", 1)[0] or fn_of[b] != c.split(".", 1)[0]:
+                raise ValueError
+        except (ValueError, AttributeError, IndexError):
+            continue
+        found.append(dict(entry=b, key=key, c=c, ret=ret.output, k=k, pairs=pairs))
+    return found
+
+
 # ---- table building ------------------------------------------------------------------------
 
 
@@ -711,6 +832,12 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
         flat = fuse_copies(flat, classes)
         flat = coalesce_copies(flat, classes)
         allocs = dead_saves(flat, classes, compiled.labels)
+    normals = {}
+    if optimize:
+        for m in match_normals(flat, classes, compiled.labels):
+            if types.get(m["c"], VType("i64")).kind == "f64" and types.get(m["ret"]) is not None \
+                    and types[m["ret"]].words == m["k"] + 1:
+                normals[m["entry"]] = m
     fused = {}
     if optimize and superblocks:
         for m in match_leapfrog(flat, classes, grad_names()):
@@ -743,6 +870,15 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
                             ins=[m["q"], m["p"], m["e"]], kind=0, width=2 * t.dim,
                             imm0=targets.index(t), imm1=m["steps"], imm2=m["head"], bits=0,
                             prim="$leapfrog", refs=[m["g"], m["i"]]))
+            terms.append((TERM_RETURN, 0, 0))
+            conds.append(None)
+            block_ops.append(ops)
+            continue
+        if bi in normals:
+            m = normals[bi]
+            ops.append(dict(opcode=OPCODES["normals"], action=ACTION_UPDATE, out=m["ret"], ins=[m["key"], m["c"]],
+                            kind=KIND_CODE[vtype(m["key"]).kind], width=m["k"] + 1, imm0=m["k"],
+                            imm1=m["pairs"], imm2=0, bits=0, prim="$normals"))
             terms.append((TERM_RETURN, 0, 0))
             conds.append(None)
             block_ops.append(ops)

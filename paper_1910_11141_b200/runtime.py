@@ -108,6 +108,7 @@ OPCODES = {
     "logpdf": 32, "grad": 33,
     "leapfrog": 64,  # fused superblock (lowering.match_leapfrog), never a source primitive
     "alloc": 65,     # push of an unobserved save (lowering.dead_saves), never a source primitive
+    "normals": 66,   # fused Box-Muller draw function (lowering.match_normals), never a source primitive
 }
 
 

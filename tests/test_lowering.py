@@ -120,3 +120,20 @@ def test_nuts_tables_shrink_and_stay_exact():
     plain = _sim_matches_oracle(cp, ins, cfg.min_stack_depth, False)
     opt = _sim_matches_oracle(cp, ins, cfg.min_stack_depth, True)
     assert opt.flat_rows * 5 < plain.flat_rows
+
+
+def test_nuts_fusions_fire():
+    """The fused momentum draw and the dead-save pass apply to NUTS-lite at every
+    dimension (odd dims leave the last pair's sine unused)."""
+    from paper_1910_11141_b200.lowering import OPCODES
+
+    for dim in (2, 5, 100):
+        cfg, t, cp = nuts_program({"dim": dim, "rho": 0.5, "config": dict(max_depth=4, iterations=2)})
+        types = infer_types(cp.flat, [vtype_of(np.zeros((1, dim))), vtype_of(np.zeros(1, np.int64))])
+        dp = lower(cp, types, optimize=True)
+        codes = set(dp.ops["opcode"].tolist())
+        assert OPCODES["normals"] in codes and OPCODES["alloc"] in codes, dim
+        nrm = dp.ops[dp.ops["opcode"] == OPCODES["normals"]][0]
+        assert (nrm["imm0"], nrm["imm1"]) == (dim, (dim + 1) // 2)
+        plain = lower(cp, types, optimize=False)
+        assert OPCODES["normals"] not in set(plain.ops["opcode"].tolist())
