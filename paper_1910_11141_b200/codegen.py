@@ -340,15 +340,17 @@ class _Gen:
             gv = bits & 0xFFFFFFFF
             gv = -1 if gv == 0xFFFFFFFF else gv
             iv = bits >> 32
+            iv = -1 if iv in (0xFFFFFFFF, -1) else iv
             grow = self.base(gv) if gv >= 0 else "-1"
-            e = ins[2]
-            return [
-                "{ ROp lf_{};",
-                f"  lf_.in_row[0] = {self.base(ins[0])}; lf_.in_row[1] = {self.base(ins[1])};",
-                f"  lf_.in_row[2] = {self.base(e)}; lf_.in_sp[2] = {int(self.vars[e]['sp']) if self.cls(e) == STACKED else -1};",
-                f"  lf_.in_w[2] = 1; lf_.out_row = {self.base(out)};",
+            irow = self.base(iv) if iv >= 0 else "-1"
+            lines = ["{ ROp lf_{};"]
+            for j, v in enumerate(ins[:3]):  # q, p (maybe forwarded stacked sources), e
+                sp = int(self.vars[v]["sp"]) if self.cls(v) == STACKED else -1
+                lines.append(f"  lf_.in_row[{j}] = {self.base(v)}; lf_.in_sp[{j}] = {sp}; lf_.in_w[{j}] = {self.w(v)};")
+            return lines + [
+                f"  lf_.out_row = {self.base(out)}; lf_.kind = {int(op['kind'])};",
                 f"  lf_.imm0 = {int(op['imm0'])}; lf_.imm1 = {int(op['imm1'])}; lf_.imm2 = {int(op['imm2'])};",
-                f"  lf_.bits = (long long)(((unsigned long long)({grow}) & 0xffffffffull) | ((unsigned long long)({self.base(iv)}) << 32));",
+                f"  lf_.bits = (long long)(((unsigned long long)({grow}) & 0xffffffffull) | ((unsigned long long)({irow}) << 32));",
                 f"  {self.leapfrog_fn(int(op['imm0']))}(a, ln, lf_, ok, sm, chain); }}",
             ]
         # gaussian grad / logpdf through DMMA

@@ -446,7 +446,8 @@ static void resolve(const ls_machine* m, std::vector<ROp>& rops, std::vector<RBl
     if (o.opcode == LS_OP_LEAPFROG) {  // side outputs as rows (g may be dead: -1)
       const int gv = (int)(o.bits & 0xffffffff), iv = (int)(o.bits >> 32);
       const long long grow = gv >= 0 ? row_of(gv) : -1;
-      r.bits = (long long)((unsigned long long)(grow & 0xffffffff) | ((unsigned long long)row_of(iv) << 32));
+      const long long irow = iv >= 0 ? row_of(iv) : -1;
+      r.bits = (long long)((unsigned long long)(grow & 0xffffffff) | ((unsigned long long)irow << 32));
     }
     rops[i] = r;
   }

@@ -591,12 +591,14 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
   __syncwarp();
   const unsigned mask = __ballot_sync(kFull, part);
   const int n = __popc(mask);
-  uint64_t* myq = part ? ln.row(op.in_row[0]) : nullptr;
-  uint64_t* myp = part ? ln.row(op.in_row[1]) : nullptr;
+  // q, p: the function's registers, or (forwarded) the caller's argument sources
+  uint64_t* myq = part ? const_cast<uint64_t*>(ln.in(op, 0)) : nullptr;
+  uint64_t* myp = part ? const_cast<uint64_t*>(ln.in(op, 1)) : nullptr;
+  const bool wb = (op.kind & 1) != 0;  // q, p read after the return: write them back
   const double mye = part ? as_f64(ln.in(op, 2)[0]) : 0.0;
   uint64_t* my_g = (part && grow >= 0) ? ln.row(grow) : nullptr;
   uint64_t* my_ret = part ? ln.row(op.out_row) : nullptr;
-  if (part) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
+  if (part && irow >= 0) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
   if (part && a.lane_trace != nullptr) {
     const int head = op.imm2;
     lane_trace_put(a, chain, head);
@@ -667,8 +669,10 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
           const int col = 8 * nt + 2 * (lane & 3) + e;
           if (col < d) {
             const uint64_t qv = f64_bits(Qs[g * SQ + col]), pv = f64_bits(p[nt][e]);
-            qo[(size_t)col * 32] = qv;
-            po[(size_t)col * 32] = pv;
+            if (wb) {
+              qo[(size_t)col * 32] = qv;
+              po[(size_t)col * 32] = pv;
+            }
             ro[(size_t)col * 32] = qv;
             ro[(size_t)(d + col) * 32] = pv;
           }
@@ -741,12 +745,13 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
   __syncwarp();
   const unsigned mask = __ballot_sync(kFull, part);
   const int n = __popc(mask);
-  uint64_t* myq = part ? ln.row(op.in_row[0]) : nullptr;  // q, p, _ret are registers
-  uint64_t* myp = part ? ln.row(op.in_row[1]) : nullptr;
+  uint64_t* myq = part ? const_cast<uint64_t*>(ln.in(op, 0)) : nullptr;
+  uint64_t* myp = part ? const_cast<uint64_t*>(ln.in(op, 1)) : nullptr;
+  const bool wb = (op.kind & 1) != 0;
   const double mye = part ? as_f64(ln.in(op, 2)[0]) : 0.0;
   uint64_t* my_g = (part && grow >= 0) ? ln.row(grow) : nullptr;
   uint64_t* my_ret = part ? ln.row(op.out_row) : nullptr;
-  if (part) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
+  if (part && irow >= 0) ln.row(irow)[0] = (uint64_t)(int64_t)steps;
   if (part && a.lane_trace != nullptr) {  // the blocks a lane walks inside the function
     const int head = op.imm2;
     lane_trace_put(a, chain, head);
@@ -815,8 +820,10 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
       uint64_t* ro = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_ret, lr);
       for (int k = lane; k < d; k += 32) {
         const uint64_t qv = f64_bits(Qs[r * SQ + k]), pv = f64_bits(Ps[r * SP + k]);
-        qo[(size_t)k * 32] = qv;
-        po[(size_t)k * 32] = pv;
+        if (wb) {
+          qo[(size_t)k * 32] = qv;
+          po[(size_t)k * 32] = pv;
+        }
         ro[(size_t)k * 32] = qv;
         ro[(size_t)(d + k) * 32] = pv;
       }

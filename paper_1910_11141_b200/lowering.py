@@ -575,6 +575,68 @@ def match_normals(flat: ir.FlatProgram, classes: dict[str, str], labels) -> list
     return found
 
 
+def superblock_io(flat: ir.FlatProgram, m: dict) -> tuple[dict, set[tuple[int, int]], int, list]:
+    """Operand forwarding and dead side outputs of a fused leapfrog function `m`.
+
+    The superblock runs immediately after its call block, so an argument copied
+    there as `A = id X; leapfrog.q = id A` (A a temporary used only for that)
+    can be read from X's current top by the superblock itself: both copies go
+    (X must not be written, pushed or popped later in the call block). The
+    function's locals q, p, g, i are written back only when some block outside
+    the function reads them. Returns ({param: source}, dropped (block, op)
+    positions, writeback flag for q/p, [g or None, i or None]).
+    """
+    body = {m["entry"], m["entry"] + 1, m["entry"] + 2, m["entry"] + 3}
+
+    def read_outside(v):
+        for bi, blk in enumerate(flat.blocks):
+            if bi in body:
+                continue
+            if isinstance(blk.terminator, ir.FlatBranch) and blk.terminator.cond == v:
+                return True
+            if any(not isinstance(o, ir.Pop) and v in o.inputs for o in blk.ops):
+                return True
+        return False
+
+    callers = [bi for bi, blk in enumerate(flat.blocks)
+               if isinstance(blk.terminator, ir.PushJump) and blk.terminator.jump_to == m["entry"]]
+    fwd, drop = {}, set()
+    for param in (m["q"], m["p"]):
+        if read_outside(param) or not callers:
+            continue
+        srcs, pos = set(), set()
+        for cb in callers:
+            ops = flat.blocks[cb].ops
+            defs = [k for k, o in enumerate(ops) if not isinstance(o, ir.Pop) and o.output == param]
+            if len(defs) != 1:
+                break
+            k = defs[0]
+            o = ops[k]
+            if not (isinstance(o, ir.Update) and o.prim.name == "id"):
+                break
+            a = o.inputs[0]
+            adefs = [j for j, x in enumerate(ops[:k]) if not isinstance(x, ir.Pop) and x.output == a]
+            uses = [j for j, x in enumerate(ops) if not isinstance(x, ir.Pop) and a in x.inputs]
+            if len(adefs) != 1 or uses != [k] or not a.split(".", 1)[-1].startswith("$a"):
+                break
+            ad = ops[adefs[0]]
+            if not (isinstance(ad, ir.Update) and ad.prim.name == "id"):
+                break
+            x = ad.inputs[0]
+            if any((isinstance(y, ir.Pop) and y.var == x) or (not isinstance(y, ir.Pop) and y.output == x)
+                   for y in ops[adefs[0] + 1:]):
+                break
+            srcs.add(x)
+            pos |= {(cb, adefs[0]), (cb, k)}
+        else:
+            if len(srcs) == 1:
+                fwd[param] = srcs.pop()
+                drop |= pos
+    writeback = int(read_outside(m["q"]) or read_outside(m["p"]))
+    refs = [m["g"] if read_outside(m["g"]) else None, m["i"] if read_outside(m["i"]) else None]
+    return fwd, drop, writeback, refs
+
+
 # ---- table building ------------------------------------------------------------------------
 
 
@@ -810,7 +872,7 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
         for op in renamed:
             d = dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]])
             if "refs" in op:  # superblock side outputs; dead temporaries are skipped (-1)
-                d["refs"] = [-1 if r in is_temp else index[r] for r in op["refs"]]
+                d["refs"] = [-1 if (r is None or r in is_temp) else index[r] for r in op["refs"]]
             out_ops.append(d)
         new_blocks.append(out_ops)
         new_conds.append(index[cond] if cond is not None else 0)
@@ -844,6 +906,10 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             t = resolve_kernel(m["grad"]).device.target
             if t is not None and t.kind == 1 and t.dim <= max_superblock_dim:
                 fused[m["entry"]] = m
+    dropped: set[tuple[int, int]] = set()
+    for m in fused.values():
+        m["fwd"], drop, m["writeback"], m["live_refs"] = superblock_io(flat, m)
+        dropped |= drop
 
     grads = grad_names()
     for n in set(types):
@@ -866,10 +932,12 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             t = resolve_kernel(m["grad"]).device.target
             if t not in targets:
                 targets.append(t)
+            # kind bit 0: write the final q, p back to the function's registers
             ops.append(dict(opcode=OPCODES["leapfrog"], action=ACTION_UPDATE, out=m["ret"],
-                            ins=[m["q"], m["p"], m["e"]], kind=0, width=2 * t.dim,
+                            ins=[m["fwd"].get(m["q"], m["q"]), m["fwd"].get(m["p"], m["p"]), m["e"]],
+                            kind=m["writeback"], width=2 * t.dim,
                             imm0=targets.index(t), imm1=m["steps"], imm2=m["head"], bits=0,
-                            prim="$leapfrog", refs=[m["g"], m["i"]]))
+                            prim="$leapfrog", refs=m["live_refs"]))
             terms.append((TERM_RETURN, 0, 0))
             conds.append(None)
             block_ops.append(ops)
@@ -887,6 +955,8 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             if isinstance(op, ir.Pop):
                 ops.append(dict(opcode=0, action=ACTION_POP, out=op.var, ins=[], kind=0, width=1,
                                 imm0=0, imm1=0, imm2=0, bits=0, prim="$pop"))
+                continue
+            if (bi, oi) in dropped:  # argument copies forwarded into a superblock
                 continue
             if (bi, oi) in allocs:
                 vt = vtype(op.output)
