@@ -349,6 +349,7 @@ class _Gen:
                 lines.append(f"  lf_.in_row[{j}] = {self.base(v)}; lf_.in_sp[{j}] = {sp}; lf_.in_w[{j}] = {self.w(v)};")
             return lines + [
                 f"  lf_.out_row = {self.base(out)}; lf_.kind = {int(op['kind'])};",
+                f"  lf_.pad = {self.base((int(op['kind']) >> 1) - 1) if int(op['kind']) >> 1 else -1};",
                 f"  lf_.imm0 = {int(op['imm0'])}; lf_.imm1 = {int(op['imm1'])}; lf_.imm2 = {int(op['imm2'])};",
                 f"  lf_.bits = (long long)(((unsigned long long)({grow}) & 0xffffffffull) | ((unsigned long long)({irow}) << 32));",
                 f"  {self.leapfrog_fn(int(op['imm0']))}(a, ln, lf_, ok, sm, chain); }}",
@@ -369,7 +370,10 @@ class _Gen:
         x = self.ptr(ins[0])
         call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], staged_B(a, {int(op['imm0'])}), part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
                 f"{'true' if want_lp else 'false'}, sm, a.lf_smem_per_warp);")
-        if want_lp:
+        if want_lp and int(op["bits"]) > 0:  # computed by the preceding superblock (fast mode)
+            lines.append(f"  if (!a.exact_logpdf) {{ if (part_) cd_[0] = ln.row({self.base(int(op['bits']) - 1)})[0]; }}")
+            lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
+        elif want_lp:
             lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
             lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
         else:

@@ -443,6 +443,11 @@ static void resolve(const ls_machine* m, std::vector<ROp>& rops, std::vector<RBl
       }
     }
     r.imm0 = o.imm0; r.imm1 = o.imm1; r.imm2 = o.imm2; r.bits = o.bits;
+    r.pad = -1;
+    // fused leaf logpdf: the superblock writes var (kind >> 1) - 1, the logpdf op
+    // reads var bits - 1 (lowering.fuse_leaf_logpdf); -1 = none
+    if (o.opcode == LS_OP_LEAPFROG && (o.kind >> 1) > 0) r.pad = row_of((o.kind >> 1) - 1);
+    if (o.opcode == LS_OP_LOGPDF && o.bits > 0) r.pad = row_of((int)o.bits - 1);
     if (o.opcode == LS_OP_LEAPFROG) {  // side outputs as rows (g may be dead: -1)
       const int gv = (int)(o.bits & 0xffffffff), iv = (int)(o.bits >> 32);
       const long long grow = gv >= 0 ? row_of(gv) : -1;

@@ -51,7 +51,8 @@ struct ROp {
   int out;                 // output (or popped) variable id, for fault reports
   int out_row, out_sp;     // output base row; stack-pointer row or -1
   int in_row[3], in_sp[3], in_w[3], in_kind[3];
-  int imm0, imm1, imm2, pad;
+  int imm0, imm1, imm2;
+  int pad;                 // fused leaf logpdf row (superblock: written, LOGPDF: read) or -1
   long long bits;          // const payload; superblock: g_row | i_row << 32 (rows, -1 = none)
 };
 
@@ -417,6 +418,12 @@ __device__ __forceinline__ const double* staged_B(const VMArgs& a, int t) {
   return (a.stage_doubles > 0 && t == a.stage_target) ? lsb_dyn_smem : nullptr;
 }
 
+// The fast gaussian logpdf from the contraction quad = q.(P q) (shared by
+// warp_gauss and the superblock's fused leaf logpdf, so both round identically).
+__device__ __forceinline__ double gauss_lp_from_quad(double norm, double quad) {
+  return __dsub_rn(norm, __dmul_rn(0.5, quad));
+}
+
 // Shared-memory row stride (doubles) of a staged 8-chain tile: DMMA A-fragment
 // loads (8 rows x 4 cols, 64-bit) are bank-conflict free.
 __host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8 * 8; return s + ((12 - s % 16) + 16) % 16; }
@@ -511,7 +518,7 @@ __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bo
     if (want_logpdf) {
       quad += __shfl_xor_sync(kFull, quad, 1);
       quad += __shfl_xor_sync(kFull, quad, 2);
-      if (src >= 0 && (lane & 3) == 0) dg[0] = f64_bits(tg.norm - 0.5 * quad);
+      if (src >= 0 && (lane & 3) == 0) dg[0] = f64_bits(gauss_lp_from_quad(tg.norm, quad));
     }
   }
   if constexpr (SX) __syncwarp();
@@ -537,7 +544,8 @@ __host__ __device__ __forceinline__ int lf_smem_doubles(int d) {
 // g = -(q P) for the tile's 8 chains, p += (e/2) g in the C-fragment layout.
 template <int NT, int C0, bool SB>
 __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
-                                        const double* Bf, double half, bool last, uint64_t* gg, int d) {
+                                        const double* Bf, double half, bool last, uint64_t* gg, int d,
+                                        bool want_lp, double& quad) {
   // LSB_LF_KC n-tiles per pass: p (in registers) + acc + prefetched fragments fit
   constexpr int NTC = (NT - C0) < LSB_LF_KC ? (NT - C0) : LSB_LF_KC;
   const int lane = threadIdx.x & 31, g = lane >> 2;
@@ -551,6 +559,8 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
       p[C0 + j][e] = __dadd_rn(__dmul_rn(half, gv), p[C0 + j][e]);
       const int col = 8 * (C0 + j) + 2 * (lane & 3) + e;
       if (last && gg != nullptr && col < d) gg[(size_t)col * 32] = f64_bits(gv);
+      // the last kick contracts at the final q: accumulate q.(P q) in warp_gauss's order
+      if (last && want_lp && col < d) quad = fma(Qs[g * SQ + col], acc[j][e], quad);
     }
   }
 }
@@ -558,15 +568,13 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
 // All passes of one kick: n-tiles C0, C0 + LSB_LF_KC, ... < NT.
 template <int NT, int C0, bool SB>
 __device__ __forceinline__ void lf_kicks(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
-                                         const double* Bf, double half, bool last, uint64_t* gg, int d) {
-  lf_kick<NT, C0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
-  if constexpr (C0 + LSB_LF_KC < NT) lf_kicks<NT, C0 + LSB_LF_KC, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+                                         const double* Bf, double half, bool last, uint64_t* gg, int d,
+                                         bool want_lp, double& quad) {
+  lf_kick<NT, C0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
+  if constexpr (C0 + LSB_LF_KC < NT)
+    lf_kicks<NT, C0 + LSB_LF_KC, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
 }
 
-// Register-momentum variant of the fused leapfrog superblock (d <= 128): p lives in
-// registers in the DMMA C-fragment layout, q in shared memory (A-fragment source).
-// Half the shared-memory footprint of the tile version, which leaves room for the
-// CTA-wide staged copy of the precision matrix's B fragments (Bf, SB = true).
 // Dev-only phase clock of the superblock (-DLSB_SB_PROFILE=1; tools/sb_profile.py):
 // [0] q staging, [1] p load, [2] kicks (DMMA), [3] drifts, [4] write-back, [5] calls
 #if LSB_SB_PROFILE
@@ -579,6 +587,12 @@ __device__ unsigned long long lsb_sb_prof[8];
 #define LSB_SB_ADD(i, t0, t1)
 #endif
 
+// Register-momentum variant of the fused leapfrog superblock (d <= 128): p lives in
+// registers in the DMMA C-fragment layout, q in shared memory (A-fragment source).
+// Half the shared-memory footprint of the tile version, which leaves room for the
+// CTA-wide staged copy of the precision matrix's B fragments (Bf, SB = true).
+// op.pad >= 0: also write the fast logpdf at the final q to that row (the
+// caller's `logpdf(q1)`, lowering.fuse_leaf_logpdf), from the last kick's DMMAs.
 template <int NT, bool SB>
 __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                  long long chain, const double* Bf) {
@@ -595,6 +609,8 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
   uint64_t* myq = part ? const_cast<uint64_t*>(ln.in(op, 0)) : nullptr;
   uint64_t* myp = part ? const_cast<uint64_t*>(ln.in(op, 1)) : nullptr;
   const bool wb = (op.kind & 1) != 0;  // q, p read after the return: write them back
+  const bool want_lp = op.pad >= 0;
+  uint64_t* my_lp = (part && want_lp) ? ln.row(op.pad) : nullptr;
   const double mye = part ? as_f64(ln.in(op, 2)[0]) : 0.0;
   uint64_t* my_g = (part && grow >= 0) ? ln.row(grow) : nullptr;
   uint64_t* my_ret = part ? ln.row(op.out_row) : nullptr;
@@ -620,6 +636,7 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
     uint64_t* gg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_g, sl);
     if (src < 0) gg = nullptr;
     const double half = __ddiv_rn(eg, 2.0);
+    double quad = 0.0;
     double p[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -638,7 +655,7 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
       for (int hs = 0; hs < 2; ++hs) {
         const bool last = (it == steps - 1) && hs == 1;
         LSB_SB_T(t_k0);
-        lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d);
+        lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
         __syncwarp();
         LSB_SB_T(t_k1);
         LSB_SB_ADD(2, t_k0, t_k1);
@@ -655,6 +672,12 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
           LSB_SB_ADD(3, t_k1, t_k2);
         }
       }
+    }
+    if (want_lp) {  // warp_gauss's reduction over the row's 4 threads
+      quad += __shfl_xor_sync(kFull, quad, 1);
+      quad += __shfl_xor_sync(kFull, quad, 2);
+      uint64_t* lo = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_lp, sl);
+      if (src >= 0 && (lane & 3) == 0) lo[0] = f64_bits(gauss_lp_from_quad(tg.norm, quad));
     }
     LSB_SB_T(t_w0);
     // write back q, p and _ret = vcat(q, p): each thread its (row, columns)

@@ -66,6 +66,12 @@ def _inplace_safe(op, var: str) -> bool:
     return var not in op.inputs
 
 
+def _registered():
+    from .workloads import registered_targets
+
+    return registered_targets()
+
+
 def grad_names() -> frozenset[str]:
     from .workloads import registered_targets
 
@@ -637,6 +643,39 @@ def superblock_io(flat: ir.FlatProgram, m: dict) -> tuple[dict, set[tuple[int, i
     return fwd, drop, writeback, refs
 
 
+def fuse_leaf_logpdf(flat: ir.FlatProgram, m: dict, logpdf_name: str, dim: int) -> tuple[int, int] | None:
+    """The caller's `logpdf(q1)` right after a fused leapfrog returns.
+
+    In NUTS-lite's leaf (reference workloads.py:388-396) the only call site's
+    return block evaluates `logpdf(vslice:0:d(leapfrog(...)))`: the log density
+    at the final position, whose contraction q.(P q) the superblock's last kick
+    has just formed. The superblock then also writes the fast logpdf (same DMMA
+    accumulators, same fma order as warp_gauss) to a register the logpdf op
+    reads when `exact_logpdf` is off. Returns (block, op) of that logpdf op.
+    """
+    callers = [bi for bi, blk in enumerate(flat.blocks)
+               if isinstance(blk.terminator, ir.PushJump) and blk.terminator.jump_to == m["entry"]]
+    rets = {flat.blocks[c].terminator.return_to for c in callers}
+    if len(rets) != 1:
+        return None
+    rb = rets.pop()
+    alias, views = {m["ret"]}, set()
+    for k, o in enumerate(flat.blocks[rb].ops):
+        if isinstance(o, ir.Pop):
+            if o.var in alias | views:
+                return None
+            continue
+        if o.prim.name == logpdf_name and len(o.inputs) == 1 and o.inputs[0] in views:
+            return rb, k
+        if o.prim.name == "id" and o.inputs[0] in alias and o.output not in alias | views:
+            alias.add(o.output)
+        elif o.prim.name == f"vslice:0:{dim}" and o.inputs[0] in alias and o.output not in alias | views:
+            views.add(o.output)
+        elif o.output in alias | views:
+            return None
+    return None
+
+
 # ---- table building ------------------------------------------------------------------------
 
 
@@ -873,6 +912,9 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
             d = dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]])
             if "refs" in op:  # superblock side outputs; dead temporaries are skipped (-1)
                 d["refs"] = [-1 if (r is None or r in is_temp) else index[r] for r in op["refs"]]
+            for key in ("lp", "cache"):  # fused leaf logpdf register
+                if key in op:
+                    d[key] = index[op[key]]
             out_ops.append(d)
         new_blocks.append(out_ops)
         new_conds.append(index[cond] if cond is not None else 0)
@@ -907,14 +949,26 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             if t is not None and t.kind == 1 and t.dim <= max_superblock_dim:
                 fused[m["entry"]] = m
     dropped: set[tuple[int, int]] = set()
+    cached_logpdf: dict[tuple[int, int], str] = {}
     for m in fused.values():
         m["fwd"], drop, m["writeback"], m["live_refs"] = superblock_io(flat, m)
         dropped |= drop
+        t = resolve_kernel(m["grad"]).device.target
+        lp_name = next((tt.logpdf for tt in _registered() if tt.grad == m["grad"]), None)
+        hit = fuse_leaf_logpdf(flat, m, lp_name, t.dim) if lp_name and (t.dim + 7) // 8 <= 16 else None
+        m["lp"] = None
+        if hit is not None:
+            m["lp"] = m["ret"].split(".", 1)[0] + ".$lp"
+            classes[m["lp"]] = "register"
+            cached_logpdf[hit] = m["lp"]
 
     grads = grad_names()
     for n in set(types):
         classes.setdefault(n, "temporary")
     extra_types: dict[str, VType] = {}
+    for m in fused.values():
+        if m.get("lp"):
+            extra_types[m["lp"]] = VType("f64")
 
     def vtype(v: str) -> VType:
         return extra_types.get(v) or types.get(v, VType("i64"))
@@ -937,7 +991,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
                             ins=[m["fwd"].get(m["q"], m["q"]), m["fwd"].get(m["p"], m["p"]), m["e"]],
                             kind=m["writeback"], width=2 * t.dim,
                             imm0=targets.index(t), imm1=m["steps"], imm2=m["head"], bits=0,
-                            prim="$leapfrog", refs=m["live_refs"]))
+                            prim="$leapfrog", refs=m["live_refs"], **({"lp": m["lp"]} if m["lp"] else {})))
             terms.append((TERM_RETURN, 0, 0))
             conds.append(None)
             block_ops.append(ops)
@@ -983,6 +1037,8 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             row = dict(opcode=dev.opcode, action=action, out=op.output, ins=list(op.inputs),
                        kind=in_kind, width=out_vt.words, imm0=imm0, imm1=imm1, imm2=0, bits=bits,
                        prim=op.prim.name)
+            if (bi, oi) in cached_logpdf:  # written by the preceding superblock (fast mode)
+                row["cache"] = cached_logpdf[(bi, oi)]
             if action == ACTION_UPDATE and op.output in op.inputs and not _inplace_safe(op, op.output):
                 tmp = f"$scratch{n_scratch}"
                 n_scratch += 1
@@ -1021,7 +1077,12 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             if "refs" in op:  # superblock side outputs: g (or -1 when dead) | i << 32
                 gref, iref = op["refs"]
                 bits = (gref & 0xFFFFFFFF) | (iref << 32)
-            op_rows.append((op["opcode"], op["action"], op["out"], len(op["ins"]), ins, op["kind"],
+            kind = op["kind"]
+            if "lp" in op:  # superblock: kind bit 0 = q/p write-back, kind >> 1 = lp var + 1
+                kind |= (op["lp"] + 1) << 1
+            if "cache" in op:  # logpdf: bits = cached value var + 1
+                bits = op["cache"] + 1
+            op_rows.append((op["opcode"], op["action"], op["out"], len(op["ins"]), ins, kind,
                             op["width"], op["imm0"], op["imm1"], op["imm2"], bits))
         g = sum(n for name, n in ref_prims[bi].items() if name in grads)
         if bi in fused:  # the superblock performs every gradient of the function's L iterations

@@ -362,3 +362,22 @@ def test_pinned_output_pool_never_overwrites_live_results(corpus_compiled):
     assert out_c.__array_interface__["data"][0] == ptr_a  # the released buffer is recycled
     want = oracle_run(cp, [a[:4096]], depth=64).output
     assert np.array_equal(out_c[:4096], want)
+
+
+def test_fused_leaf_logpdf_matches_recomputed():
+    """The superblock's fused leaf logpdf (lowering.fuse_leaf_logpdf, read by the
+    codegen build) is bit-identical to warp_gauss recomputing it (interpreter)."""
+    from paper_1910_11141_b200 import prebuilt
+
+    for kw in prebuilt.TEST_NUTS:
+        kw = dict(kw)
+        cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+        z, d = 96, t.dim
+        ins = [np.zeros((z, d)), np.arange(z, dtype=np.int64) * 7919 + 11]
+        runs = []
+        for cg in (False, "cached"):
+            got, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=cg,
+                              exact_logpdf=False, lane_trace_cap=1 << 16, return_machine=True)
+            runs.append((got, [s.copy() for s in m.lane_traces()]))
+        assert np.array_equal(runs[0][0], runs[1][0]), d
+        assert all(np.array_equal(a, b) for a, b in zip(runs[0][1], runs[1][1])), d
