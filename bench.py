@@ -95,21 +95,68 @@ def chain_keys(first: int, count: int) -> np.ndarray:
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle-reason sampling during the timed region (B200_PROFILING.md
+    clocks line): an NVML thread every 10 ms (the timed region is a few hundred ms,
+    shorter than nvidia-smi's start-up), nvidia-smi -lms as the fallback."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, device: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+
+        self.samples: list[tuple[float, float, int]] = []
+        self.proc = None
+        self.stop_evt = threading.Event()
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-i", str(device), "-lms", "200"],
-                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[device]) if vis and vis.split(",")[0].isdigit() else device
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.sample()  # the first sample is taken before the timed steps start
+            self.thread = threading.Thread(target=self.loop, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.nv = None
+            self.path = tempfile.mktemp(suffix=".csv")
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                              "-i", str(device), "-lms", "100"],
+                                             stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
+
+    def sample(self) -> None:
+        nv = self.nv
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                             float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                             int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+
+    def loop(self) -> None:
+        while not self.stop_evt.wait(0.01):
+            try:
+                self.sample()
+            except Exception:
+                return
 
     def stop(self) -> dict:
+        if self.nv is not None:
+            self.sample()  # and one after the last timed step
+            self.stop_evt.set()
+            self.thread.join()
+            reasons = sorted({name for name, attr in self.REASONS for _, _, bits in self.samples
+                              if bits & getattr(self.nv, attr, 0)})
+            return {"sm_mhz": float(np.median([s[0] for s in self.samples])),
+                    "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                    "samples": len(self.samples), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -125,7 +172,7 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples": len(rows), "source": "nvidia-smi"}
 
 
 def flush_l2(torch, dev):

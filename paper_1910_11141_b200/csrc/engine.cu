@@ -223,18 +223,21 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
   long long* bcycles = a.blk_cycles + (size_t)g * a.n_blocks;
   unsigned long long useful = 0, launched = 0;
   if (a.group_done[g]) return;
+  // the lane's chain id lives in a register; chain_of is updated whenever it changes
+  long long chain = *my_chain;
 
   for (;;) {
-    if (*my_chain == -1) {
+    if (chain == -1) {
       const unsigned long long c = atomicAdd(a.next_chain, 1ull);
       if ((long long)c < a.z) {
-        *my_chain = (long long)c;
-        init_lane(a, ln, (long long)c);
+        chain = (long long)c;
+        init_lane(a, ln, chain);
       } else {
-        *my_chain = -2;
+        chain = -2;
       }
+      *my_chain = chain;
     }
-    const int pc = *my_chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + lane] : a.halt;
+    const int pc = chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + lane] : a.halt;
     int b;
     if (a.sched == LS_SCHED_MOST_POPULATED) {
       const unsigned peers = __match_any_sync(kFull, pc);
@@ -248,31 +251,33 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       if (lane == 0) a.group_done[g] = 1;
       break;
     }
-    if (*(volatile int*)a.abort_flag) break;
+    // another group's fault stops this one within 16 steps (one flag read per 16 steps)
+    if ((steps & 15) == 0 && *(volatile int*)a.abort_flag) break;
     if (a.max_steps >= 0 && steps >= a.max_steps) {
       if (lane == 0) a.paused[0] = 1;
       break;
     }
     const bool active = pc == b;
     const int count = __popc(__ballot_sync(kFull, active));
-    if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
+    if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, b);
     StepFault f;
     const long long t_start = clock64();
-    const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, *my_chain, f, my_smem);
-    if (lane == 0) bcycles[b] += clock64() - t_start;
+    const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, chain, f, my_smem);
+    // per-block statistics as fire-and-forget reductions (no read-modify-write stall)
+    if (lane == 0) atomicAdd((unsigned long long*)&bcycles[b], (unsigned long long)(clock64() - t_start));
     const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
     const unsigned wmin = __reduce_min_sync(kFull, fkey);
     if (wmin != ~0u) {
       if (fkey == wmin) {
         // several groups may fault in one launch: the lowest chain is reported
-        const unsigned long long key = (unsigned long long)(*my_chain);
+        const unsigned long long key = (unsigned long long)chain;
         const unsigned long long old = atomicMin(&a.fault->key, key);
         if (key < old) {
           a.fault->kind = f.kind;
           a.fault->var = f.var;
           a.fault->block = b;
           a.fault->detail = f.detail;
-          a.fault->chain = *my_chain;
+          a.fault->chain = chain;
         }
         __threadfence();
         atomicExch(a.abort_flag, 1);
@@ -281,13 +286,14 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       break;
     }
     if (halted_now) {
-      write_output(a, ln, *my_chain);
+      write_output(a, ln, chain);
+      chain = -1;
       *my_chain = -1;
     }
     if (lane == 0) {
-      const int grads = a.blocks[b].grads;
-      bsteps[b] += 1;
-      bactive[b] += count;
+      const int grads = __ldg(&a.blocks[b].grads);
+      atomicAdd((unsigned long long*)&bsteps[b], 1ull);
+      atomicAdd((unsigned long long*)&bactive[b], (unsigned long long)count);
       useful += (unsigned long long)count * (unsigned long long)grads;
       launched += (unsigned long long)L * (unsigned long long)grads;
     }
