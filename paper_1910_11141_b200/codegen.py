@@ -59,7 +59,9 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # every fetch (0 = always generate)
        "interp_min": int(os.environ.get("LSB_CG_INTERP_MIN", "0")),
        # hoist constant-index element reads of unwritten storage to the segment start
-       "hoist": int(os.environ.get("LSB_CG_HOIST", "1"))}
+       "hoist": int(os.environ.get("LSB_CG_HOIST", "1")),
+       # fuse `t = x +- y` into the one or two dots that consume it
+       "ewdot": int(os.environ.get("LSB_CG_EWDOT", "1"))}
 
 
 def _u64(bits: int) -> str:
@@ -395,6 +397,76 @@ class _Gen:
             return t.kind == 1
         return False
 
+    def ew_dot_fusions(self, ops, i, j, locals_, blk) -> dict[int, list[str]]:
+        """`T = x (+|-) y` (f64 vector temporary, 8 <= width <= 128) consumed only by one or
+        two `dot(T, a)` of this segment: one pass computes both dots without storing T
+        (ew_dot; e.g. NUTS-lite's U-turn check `dq = sub(qp, qm); dot(dq, pm); dot(dq, pp)`).
+        Returns {op index: lines} — the first dot emits the fused pass, the elementwise op
+        and the second dot emit nothing."""
+        out_lines: dict[int, list[str]] = {}
+        cond = int(blk["cond"]) if int(blk["term"]) == 1 else -1
+
+        def rows(v):
+            if self.cls(v) == STACKED:
+                return None
+            r0 = int(self.vars[v]["row"])
+            return r0, r0 + max(1, self.w(v))
+
+        def clobbers(op, v):
+            """Does op (possibly) change the storage v is read from?"""
+            out, act = int(op["out"]), int(op["action"])
+            if self.cls(v) == STACKED:
+                return out == v  # a write, push or pop of v itself moves or changes its top
+            if act == POP or self.cls(out) == STACKED:
+                return False
+            ro, rv = rows(out), rows(v)
+            return ro[0] < rv[1] and rv[0] < ro[1]
+
+        for k in range(i, j):
+            op = ops[k]
+            name = OP.get(int(op["opcode"]))
+            if name not in ("add", "sub") or int(op["action"]) != UPDATE or int(op["kind"]) != F64:
+                continue
+            t, w = int(op["out"]), int(op["width"])
+            if not (8 <= w <= 128) or t in locals_ or self.cls(t) != TEMPORARY or t == cond:
+                continue
+            x, y = int(op["in"][0]), int(op["in"][1])
+            users = [m for m in range(len(ops)) if m != k and int(ops[m]["action"]) != POP
+                     and t in [int(z) for z in ops[m]["in"][:int(ops[m]["nin"])]]]
+            if not users or len(users) > 2 or any(m < k or m >= j for m in users):
+                continue
+            if any(int(ops[m]["out"]) == t for m in range(k + 1, len(ops))):
+                continue
+            dots = []
+            for m in users:
+                u = ops[m]
+                ins = [int(z) for z in u["in"][:int(u["nin"])]]
+                if OP.get(int(u["opcode"])) != "dot" or int(u["out"]) not in locals_ or ins.count(t) != 1:
+                    break
+                dots.append((m, ins[1] if ins[0] == t else ins[0], int(u["out"])))
+            else:
+                last = dots[-1][0]
+                srcs = [x, y] + [a for _, a, _ in dots]
+                if any(clobbers(ops[q], v) for q in range(k + 1, last) for v in srcs):
+                    continue
+                if any(t == a for _, a, _ in dots):
+                    continue
+                two = len(dots) == 2
+                a1 = self.ptr(dots[0][1])
+                a2 = self.ptr(dots[1][1]) if two else a1
+                code = 0 if name == "add" else 1
+                lines = ["{ double r1_, r2_;",
+                         f"  ew_dot<{w}, {code}, {'true' if two else 'false'}>({self.ptr(x)}, {self.ptr(y)}, {a1}, {a2}, r1_, r2_);",
+                         f"  s{dots[0][2]} = f64_bits(r1_);"]
+                if two:
+                    lines.append(f"  s{dots[1][2]} = f64_bits(r2_);")
+                lines.append("}")
+                out_lines[k] = []
+                out_lines[dots[0][0]] = lines
+                if two:
+                    out_lines[dots[1][0]] = []
+        return out_lines
+
     def hoistable_loads(self, ops, i, j, locals_) -> dict[int, str]:
         """Scalar element reads `s = vget(v, const)` of flat storage, issued together
         right after the last write of that storage in the segment (or at its start),
@@ -490,12 +562,15 @@ class _Gen:
             body.append("  if (ok) {")
             body += [f"    sp{r} = ln.sp_row({r});" for r in sorted(rows)]
             hoisted = self.hoistable_loads(ops, i, j, locals_) if OPT["hoist"] else {}
+            fused = self.ew_dot_fusions(ops, i, j, locals_, blk) if OPT["ewdot"] else {}
             at: dict[int, list[str]] = {}
             for k, (h, line) in hoisted.items():
                 at.setdefault(h, []).append(line)
             body += ["    " + s for s in at.get(i, [])]
             while i < j:
-                if i not in hoisted:
+                if i in fused:
+                    body += ["    " + s for s in fused[i]]
+                elif i not in hoisted:
                     body += ["    " + s for s in self.op_code(i, ops[i], locals_, i + 1)]
                 body += ["    " + s for s in at.get(i + 1, [])]
                 i += 1

@@ -166,6 +166,49 @@ __device__ __forceinline__ void select(uint64_t* dst, bool c, const uint64_t* x,
 
 // (x*y).sum(): numpy's pairwise order (lsb_ops.cuh pairwise). For a static
 // W <= 128 the whole sum is unrolled so the loads can all be issued early.
+// (x OP y).a and (x OP y).b (OP 0 = add, 1 = sub; TWO = second dot) for 8 <= W <= 128 without
+// storing x OP y: every element, product and partial sum rounds exactly as the separate
+// `t = x OP y; dot(t, a); dot(t, b)` ops (dot<W>'s numpy pairwise order), in one pass.
+template <int W, int OP, bool TWO>
+__device__ __forceinline__ void ew_dot(const uint64_t* x, const uint64_t* y, const uint64_t* a,
+                                       const uint64_t* b, double& ra, double& rb) {
+  static_assert(W >= 8 && W <= 128, "pairwise block form");
+  auto t = [&](int i) {
+    const double xv = as_f64(x[i * S]), yv = as_f64(y[i * S]);
+    return OP == 0 ? __dadd_rn(xv, yv) : __dsub_rn(xv, yv);
+  };
+  constexpr int stop = W - W % 8;
+  double r1[8], r2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double tv = t(j);
+    r1[j] = __dmul_rn(tv, as_f64(a[j * S]));
+    if (TWO) r2[j] = __dmul_rn(tv, as_f64(b[j * S]));
+  }
+#pragma unroll
+  for (int i = 8; i < stop; i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double tv = t(i + j);
+      r1[j] = __dadd_rn(r1[j], __dmul_rn(tv, as_f64(a[(i + j) * S])));
+      if (TWO) r2[j] = __dadd_rn(r2[j], __dmul_rn(tv, as_f64(b[(i + j) * S])));
+    }
+  double s1 = __dadd_rn(__dadd_rn(__dadd_rn(r1[0], r1[1]), __dadd_rn(r1[2], r1[3])),
+                        __dadd_rn(__dadd_rn(r1[4], r1[5]), __dadd_rn(r1[6], r1[7])));
+  double s2 = 0.0;
+  if (TWO)
+    s2 = __dadd_rn(__dadd_rn(__dadd_rn(r2[0], r2[1]), __dadd_rn(r2[2], r2[3])),
+                   __dadd_rn(__dadd_rn(r2[4], r2[5]), __dadd_rn(r2[6], r2[7])));
+#pragma unroll
+  for (int i = stop; i < W; ++i) {
+    const double tv = t(i);
+    s1 = __dadd_rn(s1, __dmul_rn(tv, as_f64(a[i * S])));
+    if (TWO) s2 = __dadd_rn(s2, __dmul_rn(tv, as_f64(b[i * S])));
+  }
+  ra = __dadd_rn(0.0, s1);
+  rb = __dadd_rn(0.0, s2);
+}
+
 // Shared out-of-line (x*y).sum() for 8 <= w <= 128 in numpy's pairwise order,
 // 16 products loaded per batch.
 __device__ __noinline__ double dot_n(const uint64_t* x, const uint64_t* y, int w) {
