@@ -505,6 +505,13 @@ class _Gen:
                 continue
             e = min(max(consts[idx], 0), self.w(src) - 1)
             out_lines[k] = (h, f"s{out} = ln.row({r0})[{e} * S];")
+        # sliding window: a load is issued at most kWindow hoisted loads ahead of its use
+        # (hoisting all of e.g. 100 element reads at once spills them to local memory)
+        window = 16
+        ks = sorted(out_lines)
+        for m in range(window, len(ks)):
+            h, line = out_lines[ks[m]]
+            out_lines[ks[m]] = (max(h, ks[m - window] + 1), line)
         return out_lines
 
     def block(self, b):

@@ -164,8 +164,6 @@ __device__ __forceinline__ void select(uint64_t* dst, bool c, const uint64_t* x,
 #endif
 }
 
-// (x*y).sum(): numpy's pairwise order (lsb_ops.cuh pairwise). For a static
-// W <= 128 the whole sum is unrolled so the loads can all be issued early.
 // (x OP y).a and (x OP y).b (OP 0 = add, 1 = sub; TWO = second dot) for 8 <= W <= 128 without
 // storing x OP y: every element, product and partial sum rounds exactly as the separate
 // `t = x OP y; dot(t, a); dot(t, b)` ops (dot<W>'s numpy pairwise order), in one pass.
@@ -185,7 +183,7 @@ __device__ __forceinline__ void ew_dot(const uint64_t* x, const uint64_t* y, con
     r1[j] = __dmul_rn(tv, as_f64(a[j * S]));
     if (TWO) r2[j] = __dmul_rn(tv, as_f64(b[j * S]));
   }
-#pragma unroll
+#pragma unroll 1  // one 8-element block (up to 32 loads) per iteration: no spills
   for (int i = 8; i < stop; i += 8)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -235,6 +233,9 @@ __device__ __noinline__ double dot_n(const uint64_t* x, const uint64_t* y, int w
   return __dadd_rn(0.0, res);
 }
 
+// (x*y).sum(): numpy's pairwise order (lsb_ops.cuh pairwise); for 8 <= W <= 128 the
+// 8-accumulator block form with 16 products loaded per batch (a full unroll would
+// hoist all 2W loads and spill).
 template <int W>
 __device__ __forceinline__ double dot(const uint64_t* x, const uint64_t* y) {
 #if LSB_GEN_OOL
@@ -248,10 +249,18 @@ __device__ __forceinline__ double dot(const uint64_t* x, const uint64_t* y) {
     double r[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = p(j);
+#pragma unroll 1
+    for (int i = 8; i < stop; i += 16) {
+      double v[16];
 #pragma unroll
-    for (int i = 8; i < stop; i += 8)
+      for (int j = 0; j < 16; ++j) v[j] = (i + j < stop) ? p(i + j) : 0.0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], p(i + j));
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[j]);
+      if (i + 8 < stop) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[8 + j]);
+      }
+    }
     double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 #pragma unroll
