@@ -61,7 +61,9 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # hoist constant-index element reads of unwritten storage to the segment start
        "hoist": int(os.environ.get("LSB_CG_HOIST", "1")),
        # fuse `t = x +- y` into the one or two dots that consume it
-       "ewdot": int(os.environ.get("LSB_CG_EWDOT", "1"))}
+       "ewdot": int(os.environ.get("LSB_CG_EWDOT", "1")),
+       # one pass for several copies of the same source
+       "fanout": int(os.environ.get("LSB_CG_FANOUT", "1"))}
 
 
 def _u64(bits: int) -> str:
@@ -467,6 +469,97 @@ class _Gen:
                     out_lines[dots[1][0]] = []
         return out_lines
 
+    def copy_fanouts(self, ops, i, j, busy: set[int]) -> dict[int, list[str]]:
+        """Copies of one source (same variable, offset and width) into several flat
+        destinations in a segment — `id`, `vslice` and the parts of a `vcat` — become one
+        pass that loads each element once (copy_fan), emitted at the first copy; e.g.
+        NUTS-lite's `qm = q; qp = q; prop = q` and the leaf pack (q1, p1 three and two
+        times). Moving a later write up is allowed only when nothing in between touches
+        its destination or changes the source. Returns {op index: replacement lines}."""
+        units = []  # [k, part, dst row, src var, src offset, width]
+        for k in range(i, j):
+            if k in busy:
+                continue
+            op = ops[k]
+            name, act, out = OP.get(int(op["opcode"])), int(op["action"]), int(op["out"])
+            if act != UPDATE or self.cls(out) == STACKED:
+                continue
+            w = int(op["width"])
+            ins = [int(x) for x in op["in"][:int(op["nin"])]]
+            r0 = int(self.vars[out]["row"])
+            if name == "id" and w > 1 and not self.same_rows(out, act, ins[0], 0, 0):
+                units.append((k, 0, r0, ins[0], 0, w))
+            elif name == "vslice" and w > 1 and not self.same_rows(out, act, ins[0], 0, int(op["imm0"])):
+                units.append((k, 0, r0, ins[0], int(op["imm0"]), w))
+            elif name == "vcat":
+                wa = self.w(ins[0])
+                if wa > 1 and not self.same_rows(out, act, ins[0], 0, 0):
+                    units.append((k, 0, r0, ins[0], 0, wa))
+                if w - wa > 1 and not self.same_rows(out, act, ins[1], wa, 0):
+                    units.append((k, 1, r0 + wa, ins[1], 0, w - wa))
+        groups: dict[tuple, list] = {}
+        for u in units:
+            groups.setdefault((u[3], u[4], u[5]), []).append(u)
+
+        def span(v, off, w):
+            if self.cls(v) == STACKED:
+                return None
+            r0 = int(self.vars[v]["row"]) + off
+            return r0, r0 + w
+
+        def touches(o, lo, hi, reads=True):
+            """o writes (or, with reads, also reads) flat rows [lo, hi)."""
+            vs = [int(o["out"])] if int(o["action"]) != POP else []
+            if reads:
+                vs += [int(x) for x in o["in"][:int(o["nin"])]]
+            for v in vs:
+                sp = span(v, 0, max(1, self.w(v)))
+                if sp is not None and sp[0] < hi and lo < sp[1]:
+                    return True
+            return False
+
+        handled: dict[tuple[int, int], bool] = {}
+        emit: dict[int, list[str]] = {}
+        for (src, off, w), us in groups.items():
+            if len(us) < 2:
+                continue
+            ss = span(src, off, w)
+            first = us[0][0]
+            keep = [us[0]]
+            for u in us[1:]:
+                lo, hi = u[2], u[2] + w
+                if ss is not None and ss[0] < hi and lo < ss[1]:
+                    continue  # destination overlaps the source
+                between = ops[first + 1:u[0]]  # strictly between the group's first copy and u
+                if any(touches(o, lo, hi) for o in between):
+                    continue
+                if ss is None:
+                    if any(int(o["out"]) == src for o in between):
+                        continue
+                elif any(touches(o, ss[0], ss[1], reads=False) for o in between):
+                    continue
+                keep.append(u)
+            if len(keep) < 2:
+                continue
+            src_expr = self.ptr(src) + (f" + {off} * S" if off else "")
+            dsts = ", ".join(f"ln.row({u[2]})" for u in keep)
+            emit.setdefault(first, []).extend([f"{{ uint64_t* const d_[{len(keep)}] = {{{dsts}}};",
+                                               f"  copy_fan<{w}, {len(keep)}>({src_expr}, d_); }}"])
+            for u in keep:
+                handled[(u[0], u[1])] = True
+        out_lines: dict[int, list[str]] = {}
+        for u in units:  # ops with a handled part are replaced; their other parts copy here
+            k = u[0]
+            if not any(handled.get((k, part)) for part in (0, 1)):
+                continue
+            lines = out_lines.setdefault(k, list(emit.get(k, [])))
+            if not handled.get((u[0], u[1])):
+                src_expr = self.ptr(u[3]) + (f" + {u[4]} * S" if u[4] else "")
+                lines.append(f"copy<{u[5]}>(ln.row({u[2]}), {src_expr});")
+        for k, lines in emit.items():
+            out_lines.setdefault(k, lines)
+        return out_lines
+
     def hoistable_loads(self, ops, i, j, locals_) -> dict[int, str]:
         """Scalar element reads `s = vget(v, const)` of flat storage, issued together
         right after the last write of that storage in the segment (or at its start),
@@ -570,6 +663,9 @@ class _Gen:
             body += [f"    sp{r} = ln.sp_row({r});" for r in sorted(rows)]
             hoisted = self.hoistable_loads(ops, i, j, locals_) if OPT["hoist"] else {}
             fused = self.ew_dot_fusions(ops, i, j, locals_, blk) if OPT["ewdot"] else {}
+            if OPT["fanout"]:
+                for k, lines in self.copy_fanouts(ops, i, j, set(fused) | set(hoisted)).items():
+                    fused.setdefault(k, lines)
             at: dict[int, list[str]] = {}
             for k, (h, line) in hoisted.items():
                 at.setdefault(h, []).append(line)

@@ -137,6 +137,32 @@ __device__ __noinline__ double ool_log(double x) { return log(x); }
 __device__ __noinline__ double ool_sin(double x) { return sin(x); }
 __device__ __noinline__ double ool_cos(double x) { return cos(x); }
 
+// One source vector copied to N destinations (codegen fan-out of copies that share a
+// source): each element is loaded once and stored N times, kEw loads in flight.
+template <int W, int N>
+__device__ __forceinline__ void copy_fan(const uint64_t* src, uint64_t* const (&dst)[N]) {
+  constexpr int full = W / kEw * kEw;
+#pragma unroll 1
+  for (int i = 0; i < full; i += kEw) {
+    uint64_t v[kEw];
+#pragma unroll
+    for (int j = 0; j < kEw; ++j) v[j] = src[(i + j) * S];
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) dst[n][(i + j) * S] = v[j];
+  }
+  if constexpr (full < W) {
+    uint64_t v[W - full];
+#pragma unroll
+    for (int j = 0; j < W - full; ++j) v[j] = src[(full + j) * S];
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+#pragma unroll
+      for (int j = 0; j < W - full; ++j) dst[n][(full + j) * S] = v[j];
+  }
+}
+
 template <int W>
 __device__ __forceinline__ void fill(uint64_t* dst, uint64_t v) {
 #if LSB_GEN_OOL
