@@ -611,7 +611,7 @@ class _Gen:
         blk = self.dp.blocks[b]
         ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
         if OPT["interp_min"] and len(ops) > OPT["interp_min"]:
-            return (f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane& ln, bool active, "
+            return (f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
                     f"long long chain, StepFault& f, double* sm) {{\n"
                     f"  return exec_block<true>(a, ln, {b}, active, chain, f, sm);\n}}")
         # scalar block-local temporaries -> registers
@@ -626,7 +626,7 @@ class _Gen:
         for op in ops:  # an op that reads a coop output from memory keeps it in memory
             if self.is_coop(op):
                 locals_.discard(int(op["out"]))
-        body = [f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane& ln, bool active, "
+        body = [f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
                 f"long long chain, StepFault& f, double* sm) {{",
                 "  const int D = a.depth; (void)D; (void)sm; (void)chain;",
                 "  bool ok = active;"]

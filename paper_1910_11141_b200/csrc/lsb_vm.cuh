@@ -727,7 +727,7 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
 // One out-of-line register-momentum superblock for a target with NT n-tiles
 // (program-specialised builds call this directly: one compact body in the i-cache).
 template <int NT>
-__device__ __noinline__ void warp_leapfrog_nt(const VMArgs& a, const Lane& ln, const ROp& op, bool part,
+__device__ __noinline__ void warp_leapfrog_nt(const VMArgs& a, const Lane ln, const ROp op, bool part,
                                               double* sm, long long chain) {
   const double* Bs = staged_B(a, op.imm0);
   if (Bs) warp_leapfrog_rp<NT, true>(a, ln, op, part, sm, chain, Bs);
