@@ -63,7 +63,13 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # fuse `t = x +- y` into the one or two dots that consume it
        "ewdot": int(os.environ.get("LSB_CG_EWDOT", "1")),
        # one pass for several copies of the same source
-       "fanout": int(os.environ.get("LSB_CG_FANOUT", "1"))}
+       "fanout": int(os.environ.get("LSB_CG_FANOUT", "1")),
+       # block functions inlined into the dispatcher (no call ABI) or out of line
+       "inline": int(os.environ.get("LSB_CG_INLINE", "1"))}
+
+
+def _block_qual() -> str:
+    return "__forceinline__" if OPT["inline"] else "__noinline__"
 
 
 def _u64(bits: int) -> str:
@@ -611,7 +617,7 @@ class _Gen:
         blk = self.dp.blocks[b]
         ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
         if OPT["interp_min"] and len(ops) > OPT["interp_min"]:
-            return (f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
+            return (f"__device__ {_block_qual()} bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
                     f"long long chain, StepFault& f, double* sm) {{\n"
                     f"  return exec_block<true>(a, ln, {b}, active, chain, f, sm);\n}}")
         # scalar block-local temporaries -> registers
@@ -626,7 +632,7 @@ class _Gen:
         for op in ops:  # an op that reads a coop output from memory keeps it in memory
             if self.is_coop(op):
                 locals_.discard(int(op["out"]))
-        body = [f"__device__ __noinline__ bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
+        body = [f"__device__ {_block_qual()} bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
                 f"long long chain, StepFault& f, double* sm) {{",
                 "  const int D = a.depth; (void)D; (void)sm; (void)chain;",
                 "  bool ok = active;"]
