@@ -65,7 +65,11 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        # one pass for several copies of the same source
        "fanout": int(os.environ.get("LSB_CG_FANOUT", "1")),
        # block functions inlined into the dispatcher (no call ABI) or out of line
-       "inline": int(os.environ.get("LSB_CG_INLINE", "1"))}
+       "inline": int(os.environ.get("LSB_CG_INLINE", "1")),
+       # the superblock inlined into its block too
+       "sbinline": int(os.environ.get("LSB_CG_SBINLINE", "1")),
+       # warp_gauss (DMMA grad / fast logpdf) inlined at its call sites
+       "wginline": int(os.environ.get("LSB_CG_WGINLINE", "0"))}
 
 
 def _block_qual() -> str:
@@ -764,7 +768,8 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
            f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}",
-           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_LF_KC={OPT['lfkc']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
+           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_LF_KC={OPT['lfkc']}",
+           f"-DLSB_SB_INLINE={OPT['sbinline']}", f"-DLSB_WG_INLINE={OPT['wginline']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=str(_build.ROOT))

@@ -463,7 +463,15 @@ __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bo
 // Bs: the staged B fragments (staged_B) or nullptr. sm/sm_doubles: the warp's
 // shared-memory scratch; when it holds an 8-chain tile of x, the A operand is
 // staged there (coalesced) instead of read from the workspace per k-step.
-__device__ inline void warp_gauss(const DevTarget& tg, const double* Bs, bool part, const uint64_t* xp,
+#ifndef LSB_WG_INLINE
+#define LSB_WG_INLINE 0
+#endif
+#if LSB_WG_INLINE
+__device__ __forceinline__
+#else
+__device__ inline
+#endif
+void warp_gauss(const DevTarget& tg, const double* Bs, bool part, const uint64_t* xp,
                                   uint64_t* dst, bool want_logpdf, double* sm, int sm_doubles) {
   const bool sx = sm != nullptr && 8 * lf_stride_q(tg.dim) <= sm_doubles;
   if (Bs) {
@@ -726,8 +734,16 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
 
 // One out-of-line register-momentum superblock for a target with NT n-tiles
 // (program-specialised builds call this directly: one compact body in the i-cache).
+#ifndef LSB_SB_INLINE
+#define LSB_SB_INLINE 0
+#endif
+#if LSB_SB_INLINE
+#define LSB_SB_QUAL __forceinline__
+#else
+#define LSB_SB_QUAL __noinline__
+#endif
 template <int NT>
-__device__ __noinline__ void warp_leapfrog_nt(const VMArgs& a, const Lane ln, const ROp op, bool part,
+__device__ LSB_SB_QUAL void warp_leapfrog_nt(const VMArgs& a, const Lane ln, const ROp op, bool part,
                                               double* sm, long long chain) {
   const double* Bs = staged_B(a, op.imm0);
   if (Bs) warp_leapfrog_rp<NT, true>(a, ln, op, part, sm, chain, Bs);
