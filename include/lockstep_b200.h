@@ -211,6 +211,10 @@ int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int
    fills *st; faults are reported in st->kind, not as an error code. */
 int ls_run(ls_machine* m, int64_t max_steps, ls_status* st);
 int ls_read_output(ls_machine* m, void* host, int64_t bytes);
+/* warp engine: have the kernel write output rows straight into a page-locked buffer
+   from ls_host_alloc (overlapping the transfer with the run; host = NULL reverts to
+   device memory); ls_read_output from that buffer is then only a synchronisation */
+int ls_machine_set_output_host(ls_machine* m, void* host, int64_t bytes);
 /* device pointer of the z x width output (valid until destroy) */
 int ls_output_device(ls_machine* m, void** dev);
 /* device-to-device copy of the output (e.g. into a torch CUDA tensor for NCCL diagnostics) */
@@ -233,8 +237,8 @@ int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t c
 int ls_machine_sync(ls_machine* m);
 int ls_machine_destroy(ls_machine* m);
 
-/* page-locked host buffers: ls_read_output into one is a direct DMA (the host-side
-   output pool of the Python binding, _native.HostPool) */
+/* page-locked (and device-mapped) host buffers: ls_read_output into one is a direct
+   DMA, and ls_machine_set_output_host accepts them (_native.HostPool) */
 int ls_host_alloc(int64_t bytes, void** host);
 int ls_host_free(void* host);
 

@@ -53,6 +53,7 @@ _SIGS = {
     "ls_abi_version": ([], C.c_int),
     "ls_host_alloc": ([C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
     "ls_host_free": ([C.c_void_p], C.c_int),
+    "ls_machine_set_output_host": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_last_error": ([], C.c_char_p),
     "ls_device_count": ([C.POINTER(C.c_int32)], C.c_int),
     "ls_program_create": ([C.POINTER(ProgramDesc), C.POINTER(C.c_void_p)], C.c_int),
@@ -241,6 +242,8 @@ class MachineHandle:
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
                            int(lane_trace_cap), int(warp_groups), 0 if stage_targets else MF_NO_STAGE)
         self.lane_trace_cap = int(lane_trace_cap)
+        self.warp_groups = bool(warp_groups)
+        self._host_out: np.ndarray | None = None
         h = C.c_void_p()
         _check(self.lib.ls_machine_create(program.handle, z, depth, C.byref(opts), C.byref(h)), self.lib)
         self.handle = h
@@ -263,8 +266,27 @@ class MachineHandle:
         self._c(self.lib.ls_run(self.handle, max_steps, C.byref(st)))
         return st
 
+    def stream_output_to_host(self, width: int) -> bool:
+        """Warp engine: let the next run write its output rows straight into a pinned
+        pool buffer (the PCIe transfer overlaps the run). False if none is free."""
+        if not self.warp_groups:
+            return False
+        out = HOST_POOL.array(self.lib, (self.z, width))
+        if out is None:
+            return False
+        self._c(self.lib.ls_machine_set_output_host(self.handle, _ptr(out), out.nbytes))
+        self._host_out = out
+        return True
+
     def read_output(self, width: int, dtype) -> np.ndarray:
         """A fresh host array of the output (pinned from HOST_POOL when large)."""
+        if self._host_out is not None:  # already in host memory: synchronise, hand it over
+            out, self._host_out = self._host_out, None
+            try:
+                self._c(self.lib.ls_read_output(self.handle, _ptr(out), out.nbytes))
+            finally:
+                self._c(self.lib.ls_machine_set_output_host(self.handle, None, 0))
+            return out.view(dtype)
         out = HOST_POOL.array(self.lib, (self.z, width))
         if out is None:
             out = np.empty((self.z, width), dtype=np.uint64)

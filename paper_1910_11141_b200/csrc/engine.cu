@@ -285,10 +285,13 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       ++steps;
       break;
     }
-    if (halted_now) {
-      write_output(a, ln, chain);
-      chain = -1;
-      *my_chain = -1;
+    const unsigned hmask = __ballot_sync(kFull, halted_now);
+    if (hmask) {
+      warp_write_outputs(a, ln, hmask, chain);
+      if (halted_now) {
+        chain = -1;
+        *my_chain = -1;
+      }
     }
     if (lane == 0) {
       const int grads = __ldg(&a.blocks[b].grads);
@@ -399,6 +402,8 @@ struct ls_machine {
   std::vector<uint64_t*> inputs;
   uint64_t** d_input_ptrs = nullptr;
   uint64_t* output = nullptr;
+  void* out_host = nullptr;       // ls_machine_set_output_host: page-locked destination
+  uint64_t* out_host_dev = nullptr;  // ... and its device alias (written by the kernel)
   int out_width = 0;
   unsigned long long* counters = nullptr;  // [0] next_chain [1] useful [2] launched
   long long* group_steps = nullptr;
@@ -491,7 +496,7 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   a.z = m->z; a.depth = m->depth; a.lanes = m->lanes; a.group_rows = m->group_rows;
   a.ws = m->ws; a.sp = m->sp; a.pcs = m->pcs; a.chain_of = m->chain_of;
   a.inputs = (const uint64_t* const*)m->d_input_ptrs; a.input_width = m->d_input_width;
-  a.output = m->output;
+  a.output = m->out_host_dev ? m->out_host_dev : m->output;
   a.next_chain = m->counters + 0;
   a.refill = m->refill;
   a.sched = m->opts.sched;
@@ -919,15 +924,39 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
 int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
   if (!m) return fail(LS_EINVAL, "null machine");
   if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
+  if (m->out_host_dev) {  // the kernel wrote the rows straight into the host buffer
+    CK(cudaStreamSynchronize(m->stream));
+    if (host != m->out_host) std::memcpy(host, m->out_host, (size_t)bytes);
+    return LS_OK;
+  }
   CK(cudaMemcpyAsync(host, m->output, bytes, cudaMemcpyDeviceToHost, m->stream));
   CK(cudaStreamSynchronize(m->stream));
+  return LS_OK;
+}
+
+int ls_machine_set_output_host(ls_machine* m, void* host, int64_t bytes) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  if (!host) {
+    m->out_host = nullptr;
+    m->out_host_dev = nullptr;
+    return LS_OK;
+  }
+  if (!m->warp) return fail(LS_EINVAL, "host output needs the warp engine");
+  if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
+  void* dev = nullptr;
+  if (cudaHostGetDevicePointer(&dev, host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LS_EINVAL, "host output must be mapped page-locked memory (ls_host_alloc)");
+  }
+  m->out_host = host;
+  m->out_host_dev = (uint64_t*)dev;
   return LS_OK;
 }
 
 int ls_host_alloc(int64_t bytes, void** host) {
   if (!host || bytes <= 0) return fail(LS_EINVAL, "bad host allocation request");
   *host = nullptr;
-  if (cudaHostAlloc(host, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc(host, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
     cudaGetLastError();
     *host = nullptr;
     return fail(LS_ENOMEM, "cudaHostAlloc failed");
@@ -943,14 +972,15 @@ int ls_host_free(void* host) {
 int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
   if (!m || !dev_dst) return fail(LS_EINVAL, "null machine");
   if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
-  CK(cudaMemcpyAsync(dev_dst, m->output, bytes, cudaMemcpyDeviceToDevice, m->stream));
+  CK(cudaMemcpyAsync(dev_dst, m->out_host_dev ? m->out_host_dev : m->output, bytes, cudaMemcpyDefault,
+                     m->stream));
   CK(cudaStreamSynchronize(m->stream));
   return LS_OK;
 }
 
 int ls_output_device(ls_machine* m, void** dev) {
   if (!m || !dev) return fail(LS_EINVAL, "null machine");
-  *dev = m->output;
+  *dev = m->out_host_dev ? m->out_host_dev : m->output;
   return LS_OK;
 }
 

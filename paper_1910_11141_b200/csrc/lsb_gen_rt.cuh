@@ -99,13 +99,42 @@ __device__ __forceinline__ void copy(uint64_t* dst, const uint64_t* src) {
 #endif
 }
 
-// Copy between rows the generator proved disjoint: with __restrict__ and a static
-// width the compiler may hoist many loads ahead of the stores (memory-level
-// parallelism for the latency-bound packing copies).
+// Copy between rows the generator proved disjoint, software-pipelined: the loads of
+// batch k+1 are issued before the stores of batch k, so two batches (2 kEw words per
+// thread) are in flight instead of one round trip per batch. Only valid without
+// overlap — the loads run ahead of the stores.
 template <int W>
 __device__ __forceinline__ void copy_nr(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src) {
-#pragma unroll 32
-  for (int i = 0; i < W; ++i) dst[i * S] = src[i * S];
+  constexpr int full = W / kEw * kEw;
+  if constexpr (full >= 2 * kEw) {
+    uint64_t v[kEw];
+#pragma unroll
+    for (int j = 0; j < kEw; ++j) v[j] = src[j * S];
+#pragma unroll 1
+    for (int i = kEw; i < full; i += kEw) {
+      uint64_t u[kEw];
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) u[j] = src[(i + j) * S];
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) dst[(i - kEw + j) * S] = v[j];
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) v[j] = u[j];
+    }
+    if constexpr (full < W) {  // tail loads join the last batch's stores
+      uint64_t t[W - full];
+#pragma unroll
+      for (int j = 0; j < W - full; ++j) t[j] = src[(full + j) * S];
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) dst[(full - kEw + j) * S] = v[j];
+#pragma unroll
+      for (int j = 0; j < W - full; ++j) dst[(full + j) * S] = t[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < kEw; ++j) dst[(full - kEw + j) * S] = v[j];
+    }
+  } else {
+    ew<W>(dst, [&](int i) { return src[i * S]; });
+  }
 }
 
 // Long copies through the warp's shared-memory staging area with cp.async

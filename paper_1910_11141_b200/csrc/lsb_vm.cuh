@@ -383,6 +383,37 @@ __device__ inline void write_output(const VMArgs& a, const Lane& ln, long long c
   for (; i < w; ++i) dst[i] = src[(size_t)i * ln.L];
 }
 
+// Warp engine: the lanes in `hmask` halted this step; the whole warp writes each one's
+// output row (thread t takes words t, t+32, ...), so every store instruction is one
+// contiguous 256-byte run — which also makes a page-locked host destination
+// (ls_machine_set_output_host) cheap to write across PCIe while the kernel runs.
+__device__ __forceinline__ void warp_write_outputs(const VMArgs& a, const Lane& ln, unsigned hmask,
+                                                   long long chain) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t* mysrc = ln.top(a.output_row, a.output_sp, a.out_width);
+  const int w = a.out_width;
+  while (hmask) {
+    const int l = __ffs(hmask) - 1;
+    hmask &= hmask - 1;
+    const uint64_t* src = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)mysrc, l);
+    const long long c = __shfl_sync(kFull, chain, l);
+    uint64_t* dst = a.output + (size_t)c * w;
+    for (int i0 = 0; i0 < w; i0 += 32 * 8) {
+      uint64_t v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + 32 * j + lane;
+        if (i < w) v[j] = src[(size_t)i * ln.L];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = i0 + 32 * j + lane;
+        if (i < w) dst[i] = v[j];
+      }
+    }
+  }
+}
+
 __device__ inline void init_lane(const VMArgs& a, const Lane& ln, long long chain) {
   // data stacks hold one live slot from the start (reference pc_vm.py:180-181)
   for (int r = 0; r + 1 < a.n_sp_rows; ++r) ln.sp_row(r) = 1;

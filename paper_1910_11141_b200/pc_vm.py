@@ -327,16 +327,17 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     flat = compiled.flat
     arrays = _prepare_inputs(flat, inputs)
     z = arrays[0].shape[0]
-    types = infer_types(flat, [vtype_of(a) for a in arrays])
+    in_types = [vtype_of(a) for a in arrays]
     kind = _pick_engine(engine, z, lanes_per_group)
     if kind == "exact" and z > MAX_GROUP_LANES:
         raise ValueError(f"the exact engine holds at most {MAX_GROUP_LANES} lanes")
-    pkey = (id(compiled), tuple(map(str, (vtype_of(a) for a in arrays))), optimize, kind == "warp",
+    pkey = (id(compiled), tuple(map(str, in_types)), optimize, kind == "warp",
             codegen if kind == "warp" else False)
     hit = _PROGRAM_CACHE.get(pkey)
     if hit is not None and hit[0] is compiled:
-        dp, program = hit[1], hit[2]
+        dp, program, types = hit[1], hit[2], hit[3]
     else:
+        types = infer_types(flat, in_types)
         dp = lower(compiled, types, optimize=optimize, superblocks=(kind == "warp"))
         lib = None
         if codegen and kind == "warp":
@@ -348,7 +349,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
         program = _native.Program(dp, lib)
         if len(_PROGRAM_CACHE) >= 16:
             _PROGRAM_CACHE.pop(next(iter(_PROGRAM_CACHE)))
-        _PROGRAM_CACHE[pkey] = (compiled, dp, program)
+        _PROGRAM_CACHE[pkey] = (compiled, dp, program, types)
     exact = kind == "exact"
     if kind == "cta" and lanes_per_group is None:
         lanes_per_group = 256
@@ -495,9 +496,15 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
                      exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
                      codegen=codegen, reuse=reuse)
+    if m.engine == "warp" and observer is None and not debug:
+        # output rows go straight to a pinned host buffer while the run executes
+        m._h.stream_output_to_host(m._dp.types[m.flat.output].words)
     try:
         out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
     finally:
+        if m._h._host_out is not None:  # a fault left the buffer unclaimed
+            m._h._host_out = None
+            m._h._c(m._h.lib.ls_machine_set_output_host(m._h.handle, None, 0))
         if reuse:
             if len(_MACHINE_CACHE) >= 4:
                 _MACHINE_CACHE.pop(next(iter(_MACHINE_CACHE)))
