@@ -390,6 +390,11 @@ class _Gen:
         elif want_lp:
             lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
             lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
+        elif self.dp.targets[int(op["imm0"])].kind == 2:  # logistic regression: fused two-GEMM DMMA
+            t = int(op["imm0"])
+            lines.append(f"  if (lr_coop(a, a.targets[{t}])) {{ __syncwarp(); warp_lr_grad(a.targets[{t}], part_, "
+                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm); __syncwarp(); }}")
+            lines.append(f"  else if (part_) target_grad(a.targets[{t}], {x}, S, cd_);")
         else:
             lines.append("  __syncwarp();")
             lines.append(call)
@@ -406,7 +411,8 @@ class _Gen:
             return True
         if name in ("grad", "logpdf"):
             t = self.dp.targets[int(op["imm0"])]
-            return t.kind == 1
+            # gaussian grad/logpdf; logistic-regression grad (two-GEMM DMMA, d <= 128)
+            return t.kind == 1 or (t.kind == 2 and name == "grad" and (t.dim + 7) // 8 <= 16)
         return False
 
     def ew_dot_fusions(self, ops, i, j, locals_, blk) -> dict[int, list[str]]:
@@ -644,6 +650,7 @@ class _Gen:
             body.append("  uint64_t " + ", ".join(f"s{v} = 0" for v in sorted(locals_)) + ";")
         decl_at = len(body)
         self.cached_vars = set()
+        self.end = "seg0_end"  # a leading cooperative op formats its checks before any segment
         all_sp: set[int] = set()
         seg = 0
         i = 0

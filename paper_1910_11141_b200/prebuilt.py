@@ -32,6 +32,25 @@ TEST_NUTS = [
     dict(dim=100, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=10, iterations=3),
     dict(dim=5, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=8, iterations=4),
 ]
+# logistic-regression cases (DMMA two-GEMM gradient): gradient-only programs and one NUTS run
+LR_GRAD = [(200, 5, 7), (1000, 25, 0)]
+LR_NUTS = dict(n=200, d=5, seed=7, step_size=0.1, leaf_steps=2, max_depth=5, iterations=3)
+
+
+def lr_gradient(n: int, d: int, seed: int):
+    from . import compile_program, compile_source, logistic_regression
+
+    t = logistic_regression(n, d, seed)
+    return t, compile_program(compile_source(f"def gradient(w) {{ return {t.grad}(w); }}", "gradient"))
+
+
+def lr_nuts(n: int, d: int, seed: int, **cfg):
+    from . import compile_program, compile_source, logistic_regression, nuts_lite_source
+    from .workloads import NutsConfig
+
+    config = NutsConfig(**cfg)
+    t = logistic_regression(n, d, seed)
+    return config, t, compile_program(compile_source(nuts_lite_source(config, t), "nuts_main"))
 
 
 def specs():
@@ -45,6 +64,12 @@ def specs():
         dim, rho = kw.pop("dim"), kw.pop("rho")
         _, _, cp = nuts(dim, rho, **kw)
         out.append((f"nuts_d{dim}_T{kw['iterations']}", cp, [VType("f64", dim), I64]))
+    for n, d, seed in LR_GRAD:
+        _, cp = lr_gradient(n, d, seed)
+        out.append((f"lr_grad_{n}x{d}", cp, [VType("f64", d)]))
+    kw = dict(LR_NUTS)
+    _, t, cp = lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    out.append(("lr_nuts", cp, [VType("f64", t.dim), I64]))
     for e in corpus():
         cp = compile_program(compile_source(e.source, e.entry))
         ins = e.make_inputs(np.random.default_rng(0), 2)

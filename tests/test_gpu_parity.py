@@ -381,3 +381,29 @@ def test_fused_leaf_logpdf_matches_recomputed():
             runs.append((got, [s.copy() for s in m.lane_traces()]))
         assert np.array_equal(runs[0][0], runs[1][0]), d
         assert all(np.array_equal(a, b) for a, b in zip(runs[0][1], runs[1][1])), d
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_warp_engine_logreg_dmma_gradient(codegen):
+    """Logistic-regression gradients on the warp engine's fused two-GEMM DMMA path match the
+    reference formula (workloads.py:221-228) to 1e-12, and NUTS on that target keeps every
+    lane's pc trace equal to the oracle's."""
+    from oracle import lockstep_oracle as O
+    from paper_1910_11141_b200 import prebuilt
+
+    for n, d, seed in prebuilt.LR_GRAD:
+        t, cp = prebuilt.lr_gradient(n, d, seed)
+        w = np.random.default_rng(seed).normal(size=(77, d)) * 0.3
+        got, _ = L.run(cp, [w], depth=4, engine="warp", codegen=codegen)
+        want = O.logreg_grad(w, t.params["sx"])
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+    kw = dict(prebuilt.LR_NUTS)
+    cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    z = 64
+    ins = [np.zeros((z, t.dim)), np.arange(z, dtype=np.int64) * 7919 + 11]
+    ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+    got, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=codegen,
+                      lane_trace_cap=1 << 16, return_machine=True)
+    for lane, seq in enumerate(m.lane_traces()):
+        assert np.array_equal(seq, ref.lane_blocks[lane]), lane
+    assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
