@@ -384,17 +384,22 @@ class _Gen:
         x = self.ptr(ins[0])
         call = (f"  warp_gauss(a.targets[{int(op['imm0'])}], staged_B(a, {int(op['imm0'])}), part_, part_ ? (const uint64_t*){x} : nullptr, cd_, "
                 f"{'true' if want_lp else 'false'}, sm, a.lf_smem_per_warp);")
-        if want_lp and int(op["bits"]) > 0:  # computed by the preceding superblock (fast mode)
+        if self.dp.targets[int(op["imm0"])].kind == 2:  # logistic regression: fused DMMA pass
+            t = int(op["imm0"])
+            cond = f"!a.exact_logpdf && lr_coop(a, a.targets[{t}])" if want_lp else f"lr_coop(a, a.targets[{t}])"
+            lines.append(f"  if ({cond}) {{ __syncwarp(); warp_lr(a.targets[{t}], part_, "
+                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm, {'true' if want_lp else 'false'}); "
+                         "__syncwarp(); }")
+            if want_lp:
+                lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{t}], {x}, S, 1));")
+            else:
+                lines.append(f"  else if (part_) target_grad(a.targets[{t}], {x}, S, cd_);")
+        elif want_lp and int(op["bits"]) > 0:  # computed by the preceding superblock (fast mode)
             lines.append(f"  if (!a.exact_logpdf) {{ if (part_) cd_[0] = ln.row({self.base(int(op['bits']) - 1)})[0]; }}")
             lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
         elif want_lp:
             lines.append("  if (!a.exact_logpdf) { __syncwarp();" + call.strip() + " __syncwarp(); }")
             lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{int(op['imm0'])}], {x}, S, 1));")
-        elif self.dp.targets[int(op["imm0"])].kind == 2:  # logistic regression: fused two-GEMM DMMA
-            t = int(op["imm0"])
-            lines.append(f"  if (lr_coop(a, a.targets[{t}])) {{ __syncwarp(); warp_lr_grad(a.targets[{t}], part_, "
-                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm); __syncwarp(); }}")
-            lines.append(f"  else if (part_) target_grad(a.targets[{t}], {x}, S, cd_);")
         else:
             lines.append("  __syncwarp();")
             lines.append(call)
@@ -411,8 +416,8 @@ class _Gen:
             return True
         if name in ("grad", "logpdf"):
             t = self.dp.targets[int(op["imm0"])]
-            # gaussian grad/logpdf; logistic-regression grad (two-GEMM DMMA, d <= 128)
-            return t.kind == 1 or (t.kind == 2 and name == "grad" and (t.dim + 7) // 8 <= 16)
+            # gaussian grad/logpdf; logistic-regression grad/logpdf (fused DMMA, d <= 128)
+            return t.kind == 1 or (t.kind == 2 and (t.dim + 7) // 8 <= 16)
         return False
 
     def ew_dot_fusions(self, ops, i, j, locals_, blk) -> dict[int, list[str]]:

@@ -682,7 +682,8 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
           p->targets[op.imm0].kind == LS_TARGET_GAUSSIAN && p->targets[op.imm0].NT1 <= kLfRegMaxTiles)
         m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 8 * lf_stride_q(p->targets[op.imm0].dim));
       // DMMA logistic-regression gradients stage w the same way
-      if (op.opcode == LS_OP_GRAD && p->targets[op.imm0].kind == LS_TARGET_LOGREG && p->targets[op.imm0].NT2 <= 16)
+      if ((op.opcode == LS_OP_GRAD || op.opcode == LS_OP_LOGPDF) && p->targets[op.imm0].kind == LS_TARGET_LOGREG &&
+          p->targets[op.imm0].NT2 <= 16)
         m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 8 * lf_stride_q(p->targets[op.imm0].dim));
     }
 #if defined(LSB_GENERATED) && LSB_GEN_STAGED

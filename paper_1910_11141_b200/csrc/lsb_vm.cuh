@@ -563,18 +563,54 @@ __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bo
   if constexpr (SX) __syncwarp();
 }
 
-// Logistic-regression gradient of every participating lane on the DMMA path, as one
-// fused two-GEMM pass per 8-chain m-tile (reference workloads.py:221-228):
-//   for each block of 8 data points:  m = w sx^T (K = d)     -> C fragments
-//                                     s = sigmoid(-m)        (lr_sig, elementwise)
-//                                     G += s sx (K = 8 data) <- s re-laid out as A fragments
-//   grad = G - w
-// The margins never touch memory (FlashAttention-style fusion). w is staged as an
-// 8-chain A tile in the warp's shared memory (stage_mtile); B1 = sx^T and B2 = sx are
-// the target's fragment-ordered operands (L2-resident). NT2 = ceil(d/8) <= 16.
-template <int NT2>
-__device__ void warp_lr_grad_nt(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
-                                double* Xs) {
+// Logistic regression on the DMMA path for every participating lane, as one fused pass
+// per 8-chain m-tile over blocks of 4 x 8 data points (reference workloads.py:216-228):
+//   m = w sx^T (K = d, 4 independent n-tile accumulators, prefetched fragments) -> C frags
+//   grad:   s = sigmoid(-m) (lr_sig);  G += s sx (K = data) <- s re-laid out as A fragments
+//   logpdf: acc += logaddexp(0, -m) per thread, reduced over the row's 4 threads
+// The margins never touch memory (FlashAttention-style fusion). w is staged as an 8-chain
+// A tile in the warp's shared memory (stage_mtile); B1 = sx^T and B2 = sx are the target's
+// fragment-ordered operands (L2-resident). NT2 = ceil(d/8) <= 16.
+template <int NT2, bool LOGPDF, int NB>
+__device__ __forceinline__ void lr_block(const DevTarget& tg, const double* Xs, int SQ, int nt0, double (&G)[NT2][2],
+                                         double& lp) {
+  const int lane = threadIdx.x & 31, g = lane >> 2;
+  double acc[NB][2];
+  lsb::mtile_gemm_pf<NB, false>(acc, tg.B1, tg.KS1, tg.NT1, nt0, [&](int k) -> double { return Xs[g * SQ + k]; });
+  // thread (g, c = lane & 3) takes A2[g][k] for k = c of each GEMM2 k-step from the lane
+  // holding s[g][k] in the C layout: lane 4g + k/2, element k & 1
+  const int q0 = (lane & ~3) | ((lane & 3) >> 1), q1 = q0 + 2;
+  const bool hi = (lane & 1) != 0;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int nt = nt0 + j;
+    if (LOGPDF) {
+      // padded data points (>= n) have zero margins: skip them
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (8 * nt + 2 * (lane & 3) + e < tg.n) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -acc[j][e]));
+      continue;
+    }
+    // padded data points have zero B1 columns and zero B2 rows: harmless
+    const double s0 = lsb::lr_sig(acc[j][0]), s1 = lsb::lr_sig(acc[j][1]);
+    const double u0 = __shfl_sync(kFull, s0, q0), u1 = __shfl_sync(kFull, s1, q0);
+    const double v0 = __shfl_sync(kFull, s0, q1), v1 = __shfl_sync(kFull, s1, q1);
+    const double a0 = hi ? u1 : u0, a1 = hi ? v1 : v0;
+    const double* b0 = tg.B2 + (size_t)(2 * nt) * tg.NT2 * 32 + lane;
+    if (2 * nt < tg.KS2) {
+#pragma unroll
+      for (int k = 0; k < NT2; ++k) lsb::dmma(G[k], a0, lsb::ldg_keep(b0 + k * 32));
+    }
+    if (2 * nt + 1 < tg.KS2) {
+      const double* b1 = b0 + (size_t)tg.NT2 * 32;
+#pragma unroll
+      for (int k = 0; k < NT2; ++k) lsb::dmma(G[k], a1, lsb::ldg_keep(b1 + k * 32));
+    }
+  }
+}
+
+template <int NT2, bool LOGPDF>
+__device__ void warp_lr_nt(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst, double* Xs) {
   const int lane = threadIdx.x & 31, g = lane >> 2;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n = __popc(mask);
@@ -589,30 +625,23 @@ __device__ void warp_lr_grad_nt(const DevTarget& tg, bool part, const uint64_t* 
     double G[NT2][2];
 #pragma unroll
     for (int j = 0; j < NT2; ++j) G[j][0] = G[j][1] = 0.0;
-    // thread (g, c = lane & 3) takes A2[g][k] for k = c of each GEMM2 k-step from the
-    // lane holding s[g][k] in the C layout: lane 4g + k/2, element k & 1
-    const int q0 = (lane & ~3) | ((lane & 3) >> 1), q1 = q0 + 2;
-    const bool hi = (lane & 1) != 0;
-    for (int nt = 0; nt < tg.NT1; ++nt) {
-      double acc[1][2];
-      lsb::mtile_gemm<1>(acc, tg.B1, tg.KS1, tg.NT1, nt, [&](int k) -> double { return Xs[g * SQ + k]; });
-      // rows of padded data points (>= n) have zero B1 columns and zero B2 rows: harmless
-      const double s0 = lsb::lr_sig(acc[0][0]), s1 = lsb::lr_sig(acc[0][1]);
-      const double u0 = __shfl_sync(kFull, s0, q0), u1 = __shfl_sync(kFull, s1, q0);
-      const double v0 = __shfl_sync(kFull, s0, q1), v1 = __shfl_sync(kFull, s1, q1);
-      const double a0 = hi ? u1 : u0, a1 = hi ? v1 : v0;
-      const double* b0 = tg.B2 + (size_t)(2 * nt) * tg.NT2 * 32 + lane;
-      if (2 * nt < tg.KS2) {
-#pragma unroll
-        for (int j = 0; j < NT2; ++j) lsb::dmma(G[j], a0, lsb::ldg_keep(b0 + j * 32));
-      }
-      if (2 * nt + 1 < tg.KS2) {
-        const double* b1 = b0 + (size_t)tg.NT2 * 32;
-#pragma unroll
-        for (int j = 0; j < NT2; ++j) lsb::dmma(G[j], a1, lsb::ldg_keep(b1 + j * 32));
-      }
+    double lp = 0.0;
+    int nt0 = 0;
+    for (; nt0 + 4 <= tg.NT1; nt0 += 4) lr_block<NT2, LOGPDF, 4>(tg, Xs, SQ, nt0, G, lp);
+    switch (tg.NT1 - nt0) {
+      case 3: lr_block<NT2, LOGPDF, 3>(tg, Xs, SQ, nt0, G, lp); break;
+      case 2: lr_block<NT2, LOGPDF, 2>(tg, Xs, SQ, nt0, G, lp); break;
+      case 1: lr_block<NT2, LOGPDF, 1>(tg, Xs, SQ, nt0, G, lp); break;
+      default: break;
     }
-    if (src >= 0) {
+    if (LOGPDF) {
+      lp = __dadd_rn(lp, __shfl_xor_sync(kFull, lp, 1));
+      lp = __dadd_rn(lp, __shfl_xor_sync(kFull, lp, 2));
+      if (src >= 0 && (lane & 3) == 0) {
+        const double ww = lsb::pairwise([&](int k) { return __dmul_rn(Xs[g * SQ + k], Xs[g * SQ + k]); }, 0, d);
+        dg[0] = f64_bits(__dsub_rn(-lp, __dmul_rn(0.5, __dadd_rn(0.0, ww))));
+      }
+    } else if (src >= 0) {
 #pragma unroll
       for (int j = 0; j < NT2; ++j)
 #pragma unroll
@@ -625,17 +654,26 @@ __device__ void warp_lr_grad_nt(const DevTarget& tg, bool part, const uint64_t* 
   }
 }
 
-__device__ inline void warp_lr_grad(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
-                                    double* Xs) {
+// grad (want_logpdf = false) or fast logpdf of a logistic-regression target, DMMA path
+__device__ inline void warp_lr(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst, double* Xs,
+                               bool want_logpdf) {
   switch (tg.NT2) {
-#define LSB_LR_CASE(K) \
-  case K: warp_lr_grad_nt<K>(tg, part, xp, dst, Xs); return;
+#define LSB_LR_CASE(K)                                                   \
+  case K:                                                                \
+    if (want_logpdf) warp_lr_nt<K, true>(tg, part, xp, dst, Xs);         \
+    else warp_lr_nt<K, false>(tg, part, xp, dst, Xs);                    \
+    return;
     LSB_LR_CASE(1) LSB_LR_CASE(2) LSB_LR_CASE(3) LSB_LR_CASE(4) LSB_LR_CASE(5) LSB_LR_CASE(6)
     LSB_LR_CASE(7) LSB_LR_CASE(8) LSB_LR_CASE(9) LSB_LR_CASE(10) LSB_LR_CASE(11) LSB_LR_CASE(12)
     LSB_LR_CASE(13) LSB_LR_CASE(14) LSB_LR_CASE(15) LSB_LR_CASE(16)
 #undef LSB_LR_CASE
     default: break;
   }
+}
+
+__device__ inline void warp_lr_grad(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+                                    double* Xs) {
+  warp_lr(tg, part, xp, dst, Xs, false);
 }
 
 // LR gradients take the DMMA path when the warp's scratch holds an 8-chain tile of w
@@ -646,7 +684,9 @@ __device__ __forceinline__ bool lr_coop(const VMArgs& a, const DevTarget& tg) {
 __device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
   if (op.opcode == LS_OP_GRAD)
     return a.targets[op.imm0].kind == LS_TARGET_GAUSSIAN || lr_coop(a, a.targets[op.imm0]);
-  if (op.opcode == LS_OP_LOGPDF) return !a.exact_logpdf && a.targets[op.imm0].kind == LS_TARGET_GAUSSIAN;
+  if (op.opcode == LS_OP_LOGPDF)
+    return !a.exact_logpdf &&
+           (a.targets[op.imm0].kind == LS_TARGET_GAUSSIAN || lr_coop(a, a.targets[op.imm0]));
   return false;
 }
 
@@ -1034,7 +1074,8 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
       if (WARP) {
         __syncwarp();
         if (a.targets[op.imm0].kind == LS_TARGET_LOGREG)
-          warp_lr_grad(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, lf_smem);
+          warp_lr(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, lf_smem,
+                  op.opcode == LS_OP_LOGPDF);
         else
           warp_gauss(a.targets[op.imm0], staged_B(a, op.imm0), part, part ? ln.in(op, 0) : nullptr, dst,
                      op.opcode == LS_OP_LOGPDF, lf_smem, a.lf_smem_per_warp);

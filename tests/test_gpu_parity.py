@@ -407,3 +407,18 @@ def test_warp_engine_logreg_dmma_gradient(codegen):
     for lane, seq in enumerate(m.lane_traces()):
         assert np.array_equal(seq, ref.lane_blocks[lane]), lane
     assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
+
+
+def test_warp_engine_logreg_fast_logpdf():
+    """Fast mode (exact_logpdf=False): the fused DMMA logistic-regression logpdf agrees with
+    the reference formula (workloads.py:216-219) to 1e-12 relative."""
+    from oracle import lockstep_oracle as O
+    from paper_1910_11141_b200 import prebuilt
+
+    for n, d, seed in prebuilt.LR_GRAD:
+        t = L.logistic_regression(n, d, seed)
+        cp = L.compile_program(L.compile_source(f"def lp(w) {{ return {t.logpdf}(w); }}", "lp"))
+        w = np.random.default_rng(seed + 1).normal(size=(77, d)) * 0.3
+        got, _ = L.run(cp, [w], depth=4, engine="warp", exact_logpdf=False)
+        want = O.logreg_logpdf(w, t.params["sx"])
+        np.testing.assert_allclose(got, want, rtol=1e-12)
