@@ -55,6 +55,7 @@ struct CtaShared {
 };
 
 __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant__ VMArgs a) {
+#ifndef LSB_GENERATED  // program-specialised libraries run the warp engine only
   extern __shared__ int s_hist[];  // [n_blocks + 1]
   __shared__ CtaShared sh;
   const int g = blockIdx.x;
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
     if (useful) atomicAdd(a.useful, useful);
     if (launched) atomicAdd(a.launched, launched);
   }
+#endif
 }
 
 // up to 16 warps per CTA (one CTA per SM when a target is staged); 128 registers
@@ -669,6 +671,12 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int groups;
   m->warp = m->opts.warp_groups != 0;
+#ifdef LSB_GENERATED
+  if (!m->warp) {
+    delete m;
+    return fail(LS_EINVAL, "a program-specialised library runs the warp engine only");
+  }
+#endif
   if (m->warp) {
     // one 32-lane group per warp, 4 warps per CTA; default: a group per 32 chains,
     // capped at the warps that are resident at once (persistent CTAs refill chains)

@@ -88,6 +88,9 @@ def build_all(workers: int = 8, verbose: bool = False) -> list:
     from .pc_vm import infer_types
 
     dps = [lower(cp, infer_types(cp.flat, ts), optimize=True, superblocks=True) for _, cp, ts in specs()]
+    # longest compiles first (ptxas time grows with the program's op count and DMMA
+    # call sites): the pool's makespan is then close to total / workers
+    dps.sort(key=lambda dp: -(len(dp.ops) + 400 * sum(t.kind == 2 for t in dp.targets)))
     with ThreadPoolExecutor(workers) as ex:
         paths = list(ex.map(lambda dp: codegen.library_for(dp, verbose=verbose), dps))
     keep = {p.name for p in paths}
