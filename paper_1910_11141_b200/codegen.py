@@ -633,8 +633,12 @@ class _Gen:
         ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
         if OPT["interp_min"] and len(ops) > OPT["interp_min"]:
             return (f"__device__ {_block_qual()} bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
-                    f"long long chain, StepFault& f, double* sm) {{\n"
-                    f"  return exec_block<true>(a, ln, {b}, active, chain, f, sm);\n}}")
+                    f"long long chain, StepFault& f, double* sm, int& pc_, int& psp_) {{\n"
+                    f"  int& msp_ = ln.sp_row(a.n_sp_rows - 1);  // the interpreter keeps pc state in memory\n"
+                    f"  msp_ = psp_; ln.pcs[(psp_ - 1) * ln.L + ln.t] = pc_;\n"
+                    f"  const bool h_ = exec_block<true>(a, ln, {b}, active, chain, f, sm);\n"
+                    f"  psp_ = msp_; if (psp_ >= 1) pc_ = ln.pcs[(psp_ - 1) * ln.L + ln.t];\n"
+                    f"  return h_;\n}}")
         # scalar block-local temporaries -> registers
         locals_ = set()
         for op in ops:
@@ -648,7 +652,7 @@ class _Gen:
             if self.is_coop(op):
                 locals_.discard(int(op["out"]))
         body = [f"__device__ {_block_qual()} bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
-                f"long long chain, StepFault& f, double* sm) {{",
+                f"long long chain, StepFault& f, double* sm, int& pc_, int& psp_) {{",
                 "  const int D = a.depth; (void)D; (void)sm; (void)chain;",
                 "  bool ok = active;"]
         if locals_:
@@ -718,7 +722,7 @@ class _Gen:
             body.append(f"  const bool cond_ = {cv} != 0;")
         else:
             body.append("  const bool cond_ = false;")
-        body.append(f"  return finish_block(a, ln, {term}, {ta}, {tb}, cond_, {int(blk['op_count']) + 1}, f);")
+        body.append(f"  return finish_block(a, ln, {term}, {ta}, {tb}, cond_, {int(blk['op_count']) + 1}, f, pc_, psp_);")
         body.append("}")
         return "\n".join(body)
 
@@ -729,30 +733,33 @@ class _Gen:
                f"#define LSB_GEN_STAGED {int(OPT['staged'])}",
                f"#define LSB_GEN_OOL {int(OPT['ool'])}",
                '#include "lsb_gen_rt.cuh"', "namespace lsbgen {",
+               "// The current pc and pc-stack pointer live in registers (the engine writes them",
+               "// back when a launch ends); memory keeps only the return addresses below the top.",
                "__device__ __forceinline__ bool finish_block(const VMArgs& a, const Lane& ln, int term, int ta, int tb,",
-               "                                             bool cond, int pos, StepFault& f) {",
-               "  int& psp = ln.sp_row(a.n_sp_rows - 1);",
-               "  int* top = &ln.pcs[(psp - 1) * ln.L + ln.t];",
+               "                                             bool cond, int pos, StepFault& f, int& pc, int& psp) {",
                "  switch (term) {",
-               "    case LS_JUMP: *top = ta; return false;",
-               "    case LS_BRANCH: *top = cond ? ta : tb; return false;",
+               "    case LS_JUMP: pc = ta; return false;",
+               "    case LS_BRANCH: pc = cond ? ta : tb; return false;",
                "    case LS_PUSHJUMP:",
-               "      *top = tb;",
-               "      if (psp >= a.depth + 1) { f = StepFault{pos, LS_RUN_OVERFLOW, -1, 0}; return false; }",
-               "      ln.pcs[psp * ln.L + ln.t] = ta; ++psp; return false;",
+               "      ln.pcs[(psp - 1) * ln.L + ln.t] = tb;",
+               "      if (psp >= a.depth + 1) { pc = tb; f = StepFault{pos, LS_RUN_OVERFLOW, -1, 0}; return false; }",
+               "      ++psp; pc = ta; return false;",
                "    default:",
                "      if (psp < 1) { f = StepFault{pos, LS_RUN_UNDERFLOW, -1, 0}; return false; }",
                "      --psp;",
-               "      return psp >= 1 && ln.pcs[(psp - 1) * ln.L + ln.t] == a.halt;",
+               "      if (psp < 1) return false;",
+               "      pc = ln.pcs[(psp - 1) * ln.L + ln.t];",
+               "      return pc == a.halt;",
                "  }",
                "}"]
         for b in range(n):
             out.append(self.block(b))
         out.append("__device__ __forceinline__ bool gen_exec_block(const VMArgs& a, const Lane& ln, int b, bool active,")
-        out.append("                                               long long chain, StepFault& f, double* sm) {")
+        out.append("                                               long long chain, StepFault& f, double* sm,")
+        out.append("                                               int& pc_, int& psp_) {")
         out.append("  switch (b) {")
         for b in range(n):
-            out.append(f"    case {b}: return gb_{b}(a, ln, active, chain, f, sm);")
+            out.append(f"    case {b}: return gb_{b}(a, ln, active, chain, f, sm, pc_, psp_);")
         out.append("  }")
         out.append("  return false;")
         out.append("}")

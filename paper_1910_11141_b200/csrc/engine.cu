@@ -35,7 +35,6 @@
 // interpreter with generated straight-line block functions.
 #ifdef LSB_GENERATED
 #include LSB_GENERATED
-#define LSB_WARP_EXEC(...) lsbgen::gen_exec_block(__VA_ARGS__)
 #else
 #define LSB_WARP_EXEC(...) exec_block<true>(__VA_ARGS__)
 #endif
@@ -227,6 +226,15 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
   if (a.group_done[g]) return;
   // the lane's chain id lives in a register; chain_of is updated whenever it changes
   long long chain = *my_chain;
+#ifdef LSB_GENERATED
+  // generated blocks keep the current pc and the pc-stack pointer in registers; memory
+  // holds the return addresses below the top and is brought up to date when we leave
+  int pc_r = a.halt, psp_r = 0;
+  if (chain >= 0) {
+    psp_r = *pc_sp;
+    pc_r = ln.pcs[(psp_r - 1) * L + lane];
+  }
+#endif
 
   for (;;) {
     if (chain == -1) {
@@ -234,12 +242,20 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       if ((long long)c < a.z) {
         chain = (long long)c;
         init_lane(a, ln, chain);
+#ifdef LSB_GENERATED
+        psp_r = 2;  // init_lane seeded the pc stack [halt, entry]
+        pc_r = a.entry;
+#endif
       } else {
         chain = -2;
       }
       *my_chain = chain;
     }
+#ifdef LSB_GENERATED
+    const int pc = chain >= 0 ? pc_r : a.halt;
+#else
     const int pc = chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + lane] : a.halt;
+#endif
     int b;
     if (a.sched == LS_SCHED_MOST_POPULATED) {
       const unsigned peers = __match_any_sync(kFull, pc);
@@ -264,7 +280,11 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
     if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, b);
     StepFault f;
     const long long t_start = clock64();
+#ifdef LSB_GENERATED
+    const bool halted_now = lsbgen::gen_exec_block(a, ln, b, active, chain, f, my_smem, pc_r, psp_r);
+#else
     const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, chain, f, my_smem);
+#endif
     // per-block statistics as fire-and-forget reductions (no read-modify-write stall)
     if (lane == 0) atomicAdd((unsigned long long*)&bcycles[b], (unsigned long long)(clock64() - t_start));
     const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
@@ -304,6 +324,12 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
     }
     ++steps;
   }
+#ifdef LSB_GENERATED
+  if (chain >= 0) {  // paused, aborted or faulted with a live chain: pc state back to memory
+    ln.pcs[(psp_r - 1 < 0 ? 0 : psp_r - 1) * L + lane] = pc_r;
+    *pc_sp = psp_r;
+  }
+#endif
   if (lane == 0) {
     a.group_steps[g] = steps;
     if (useful) atomicAdd(a.useful, useful);
