@@ -463,13 +463,14 @@ __host__ __device__ __forceinline__ int lf_stride_q(int d) { int s = (d + 7) / 8
 // missing chains) into Xs[8][SQ]. Thread (k % 4, row r) reads x[k][lane_r], so each
 // load instruction covers 4 workspace rows x 8 lanes (64-byte runs when the lanes
 // are contiguous), 8 loads in flight per thread.
+// kBatch loads in flight per thread; the superblock passes its whole tile (one round trip).
+template <int kBatch = 8>
 __device__ __forceinline__ void stage_mtile(double* Xs, int SQ, const uint64_t* myx, unsigned mask, int n,
                                             int mt, int d) {
   const int lane = threadIdx.x & 31;
   const int r = lane & 7, kq = lane >> 3;
   const int lr = mtile_lane(mask, n, mt, r);
   const uint64_t* xg = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)myx, lr < 0 ? 0 : lr);
-  constexpr int kBatch = 8;
   for (int k0 = 0; k0 < SQ; k0 += 4 * kBatch) {
     double v[kBatch];
 #pragma unroll
@@ -786,7 +787,7 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
   }
   for (int mt = 0; mt * 8 < n; ++mt) {
     LSB_SB_T(t_a);
-    stage_mtile(Qs, SQ, myq, mask, n, mt, d);  // q of the m-tile's 8 chains
+    stage_mtile<(8 * NT + 16 + 3) / 4>(Qs, SQ, myq, mask, n, mt, d);  // q of the m-tile's 8 chains, one round trip
     LSB_SB_T(t_b);
     LSB_SB_ADD(0, t_a, t_b);
     const int src = mtile_lane(mask, n, mt, g);
