@@ -137,3 +137,27 @@ def test_nuts_fusions_fire():
         assert (nrm["imm0"], nrm["imm1"]) == (dim, (dim + 1) // 2)
         plain = lower(cp, types, optimize=False)
         assert OPCODES["normals"] not in set(plain.ops["opcode"].tolist())
+
+
+def test_superblock_forwarding_and_fused_leaf_logpdf():
+    """With superblocks the leapfrog reads its arguments from the caller's sources (the call
+    block's argument copies disappear), writes back nothing the program never reads, and
+    fills the register the leaf's logpdf reads in fast mode."""
+    from paper_1910_11141_b200.lowering import OPCODES
+
+    cfg, t, cp = nuts_program({"dim": 100, "rho": 0.5, "config": dict(max_depth=6, iterations=2)})
+    types = infer_types(cp.flat, [vtype_of(np.zeros((1, 100))), vtype_of(np.zeros(1, np.int64))])
+    dp = lower(cp, types, optimize=True, superblocks=True)
+    (lf,) = dp.ops[dp.ops["opcode"] == OPCODES["leapfrog"]]
+    names = [dp.var_names[int(v)] for v in lf["in"][:2]]
+    assert names == ["build_tree.q", "build_tree.p"]  # forwarded from the caller
+    assert int(lf["kind"]) & 1 == 0  # q, p are dead after the return: no write-back
+    assert int(lf["bits"]) == -1  # g and i are dead too
+    lp_var = (int(lf["kind"]) >> 1) - 1
+    assert dp.var_names[lp_var] == "leapfrog.$lp"
+    cached = dp.ops[(dp.ops["opcode"] == OPCODES["logpdf"]) & (dp.ops["bits"] > 0)]
+    assert len(cached) == 1 and int(cached[0]["bits"]) - 1 == lp_var
+    # the call block (build_tree.b1) no longer copies vectors into leapfrog.q / leapfrog.p
+    call = dp.blocks[cp.labels.index("build_tree.b1")]
+    ops = dp.ops[call["op_begin"]:call["op_begin"] + call["op_count"]]
+    assert not any(dp.var_names[int(o["out"])] in ("leapfrog.q", "leapfrog.p") for o in ops)
