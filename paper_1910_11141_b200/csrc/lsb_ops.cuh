@@ -55,33 +55,74 @@ __device__ __forceinline__ double rng_uniform(int64_t key, int64_t ctr) {
   return __dmul_rn((double)(z >> 11), 1.0 / 9007199254740992.0);
 }
 
-// numpy pairwise_sum (unroll 8, block 128) over p(i), i in [lo, lo+n).
+// numpy pairwise_sum leaf (unroll 8, block 128) over p(i), i in [lo, lo+n), n <= 128.
 template <class P>
-__device__ double pairwise(const P& p, int lo, int n) {
+__device__ __forceinline__ double pairwise_leaf(const P& p, int lo, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, p(lo + i));
     return r;
   }
-  if (n <= 128) {
-    double r0 = p(lo + 0), r1 = p(lo + 1), r2 = p(lo + 2), r3 = p(lo + 3);
-    double r4 = p(lo + 4), r5 = p(lo + 5), r6 = p(lo + 6), r7 = p(lo + 7);
-    int i = 8;
-    const int stop = n - (n % 8);
-    for (; i < stop; i += 8) {
-      r0 = __dadd_rn(r0, p(lo + i + 0)); r1 = __dadd_rn(r1, p(lo + i + 1));
-      r2 = __dadd_rn(r2, p(lo + i + 2)); r3 = __dadd_rn(r3, p(lo + i + 3));
-      r4 = __dadd_rn(r4, p(lo + i + 4)); r5 = __dadd_rn(r5, p(lo + i + 5));
-      r6 = __dadd_rn(r6, p(lo + i + 6)); r7 = __dadd_rn(r7, p(lo + i + 7));
-    }
-    double r = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-    for (; i < n; ++i) r = __dadd_rn(r, p(lo + i));
-    return r;
+  double r0 = p(lo + 0), r1 = p(lo + 1), r2 = p(lo + 2), r3 = p(lo + 3);
+  double r4 = p(lo + 4), r5 = p(lo + 5), r6 = p(lo + 6), r7 = p(lo + 7);
+  int i = 8;
+  const int stop = n - (n % 8);
+  for (; i < stop; i += 8) {
+    r0 = __dadd_rn(r0, p(lo + i + 0)); r1 = __dadd_rn(r1, p(lo + i + 1));
+    r2 = __dadd_rn(r2, p(lo + i + 2)); r3 = __dadd_rn(r3, p(lo + i + 3));
+    r4 = __dadd_rn(r4, p(lo + i + 4)); r5 = __dadd_rn(r5, p(lo + i + 5));
+    r6 = __dadd_rn(r6, p(lo + i + 6)); r7 = __dadd_rn(r7, p(lo + i + 7));
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise(p, lo, n2), pairwise(p, lo + n2, n - n2));
+  double r = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                       __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) r = __dadd_rn(r, p(lo + i));
+  return r;
+}
+
+// numpy pairwise_sum over p(i), i in [lo, lo+n): blocks of <= 128 summed by
+// pairwise_leaf, split at n2 = n/2 rounded down to a multiple of 8, left + right.
+// The split tree is walked with an explicit stack (device recursion would put
+// frames on the per-thread call stack, which overflows inside the VM kernels once
+// n > 256); every addition happens in the recursive form's order. Out of line:
+// one small frame, and the VM kernels do not inline a copy per call site.
+template <class P>
+__device__ __noinline__ double pairwise_split(const P& p, int lo, int n) {
+  constexpr int kDepth = 32;  // n - n2 <= n/2 + 8: depth < 31 for any int n
+  int s_lo[kDepth], s_n[kDepth];
+  double s_left[kDepth];
+  bool s_right[kDepth];
+  int sp = 0;
+  s_lo[0] = lo, s_n[0] = n, s_right[0] = false;
+  for (;;) {
+    // descend through left children to a leaf
+    while (s_n[sp] > 128) {
+      int n2 = s_n[sp] / 2;
+      n2 -= n2 % 8;
+      s_lo[sp + 1] = s_lo[sp], s_n[sp + 1] = n2, s_right[sp + 1] = false;
+      ++sp;
+    }
+    double r = pairwise_leaf(p, s_lo[sp], s_n[sp]);
+    // climb: a finished left child starts its sibling; a finished right child combines
+    for (;;) {
+      if (sp == 0) return r;
+      const bool was_right = s_right[sp];
+      --sp;
+      if (!was_right) {
+        int n2 = s_n[sp] / 2;
+        n2 -= n2 % 8;
+        s_left[sp] = r;
+        s_lo[sp + 1] = s_lo[sp] + n2, s_n[sp + 1] = s_n[sp] - n2, s_right[sp + 1] = true;
+        ++sp;
+        break;
+      }
+      r = __dadd_rn(s_left[sp], r);
+    }
+  }
+}
+
+template <class P>
+__device__ __forceinline__ double pairwise(const P& p, int lo, int n) {
+  return n <= 128 ? pairwise_leaf(p, lo, n) : pairwise_split(p, lo, n);
 }
 
 struct StridedProd {

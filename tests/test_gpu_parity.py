@@ -422,3 +422,39 @@ def test_warp_engine_logreg_fast_logpdf():
         got, _ = L.run(cp, [w], depth=4, engine="warp", exact_logpdf=False)
         want = O.logreg_logpdf(w, t.params["sx"])
         np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+# ---- BASELINE config 5: ill-conditioned 1000-d gaussian, max_tree_depth 15 ------------------
+
+
+@pytest.fixture(scope="module")
+def illcond_programs():
+    """rho = 9999/10999 at d = 1000: covariance eigenvalues 1000/10999 and 10000000/10999,
+    condition number 1e4. Step sizes: 0.02 grows deep trees, 0.25 is the
+    bench setting, 0.7 puts eps*omega_max above 2 so every trajectory diverges."""
+    t = L.correlated_gaussian(1000, 9999 / 10999)
+    ev = np.linalg.eigvalsh(t.cov)
+    assert abs(ev.max() / ev.min() - 1e4) < 1e-6 * 1e4
+    out = {}
+    for eps in (0.02, 0.25, 0.7):
+        cfg = L.NutsConfig(step_size=eps, leaf_steps=4, max_depth=15, iterations=3, seed=0)
+        out[eps] = (cfg, t, L.compile_program(L.compile_source(L.nuts_lite_source(cfg, t), "nuts_main")))
+    return out
+
+
+@pytest.mark.parametrize("engine", ["exact", "warp"])
+@pytest.mark.parametrize("eps", [0.02, 0.25, 0.7])
+def test_illconditioned_1000d_depth15_lanes_exact(illcond_programs, eps, engine):
+    cfg, t, cp = illcond_programs[eps]
+    z, d = 32, t.dim
+    ins = [np.zeros((z, d)), np.arange(z, dtype=np.int64) * 7919 + 11]
+    ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+    got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine=engine, lane_trace_cap=1 << 16,
+                       return_machine=True)
+    # every tree depth, divergence exit and accept decision is the oracle's
+    for lane, seq in enumerate(m.lane_traces()):
+        assert np.array_equal(seq, ref.lane_blocks[lane]), (eps, lane)
+    # at eps 0.7 only positions that passed the divergence test reach the chain
+    assert np.isfinite(got).all()
+    assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
+    assert m.useful_grads == tr.useful_invocations({t.grad}) > 0
