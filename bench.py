@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--groups", type=int, default=0, help="persistent CTAs (0 = auto)")
     ap.add_argument("--exact-logpdf", action="store_true",
                     help="numpy einsum summation order for logpdf (default: DMMA form, 1e-15 rel)")
-    ap.add_argument("--schedule", default="min_pc", choices=("min_pc", "most_populated"))
+    ap.add_argument("--schedule", default="priority", choices=("min_pc", "most_populated", "local", "priority"),
+                    help="block selection (paper_1910_11141_b200/schedule.py); lanes never depend on it")
     ap.add_argument("--no-codegen", action="store_true",
                     help="warp engine with the op interpreter instead of specialised block code")
     ap.add_argument("--no-e2e", action="store_true")
@@ -291,6 +292,10 @@ def main():
     mach = _native.MachineHandle(prog, z, cfg.min_stack_depth, sched=args.schedule,
                                  lanes_per_cta=0 if warp else args.lanes, ctas=args.groups,
                                  exact_logpdf=args.exact_logpdf, warp_groups=warp)
+    from paper_1910_11141_b200.schedule import block_keys
+
+    mach.set_block_keys(block_keys(cp.flat, cp.labels, args.schedule,
+                                   np.flatnonzero(np.asarray(dp.blocks["grads"]) > 0)))
     # inputs resident in HBM before the timed region
     q0_d = torch.zeros((z, args.dim), dtype=torch.float64, device=dev)
     key_d = torch.from_numpy(key).to(dev)

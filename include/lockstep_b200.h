@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define LS_ABI_VERSION 1
+#define LS_ABI_VERSION 2
 
 /* ---- status codes ---------------------------------------------------------- */
 enum {
@@ -105,6 +105,11 @@ enum { LS_TARGET_GAUSSIAN = 1, LS_TARGET_LOGREG = 2 };
 enum {
   LS_SCHED_MIN_PC = 0,          /* reference rule: lowest populated block (pc_vm.py:306-311) */
   LS_SCHED_MOST_POPULATED = 1,  /* paper's throughput rule: block with most live lanes        */
+  LS_SCHED_LOCAL = 2,           /* Alg. 1 local-static batching (reference local_exec.run_local):
+                                   the deepest activation runs first, return landing pads first
+                                   within it, then the lowest block (keys from the host)        */
+  LS_SCHED_PRIORITY = 3,        /* least host-given block key (ls_machine_set_block_keys), e.g.
+                                   reverse post-order with contraction blocks deferred          */
 };
 
 /* One flat op (ir.Push/Update/Pop). */
@@ -191,6 +196,10 @@ typedef struct ls_machine ls_machine;
 int ls_abi_version(void);
 const char* ls_last_error(void);
 int ls_device_count(int32_t* n);
+/* Select the CUDA device later ls_program_create / ls_machine_create calls of this host
+   thread allocate on (one process per GPU: rank r passes its LOCAL_RANK). Programs and
+   machines remember their device; every later call on them runs there. */
+int ls_set_device(int32_t device);
 
 int ls_program_create(const ls_program_desc* desc, ls_program** out);
 /* Bind target slot `slot`: gaussian params = P (dim x dim, row-major) and
@@ -205,6 +214,10 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth,
 int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes);
 /* rewind a machine to its freshly-seeded state (inputs kept), without reallocating */
 int ls_machine_reset(ls_machine* m);
+/* keyed schedule rules (min_pc, local, priority): the least keys[b] among live lanes' blocks
+   runs next; bits 0..15 of keys[b] must equal b (the local rule uses bits 0..23). Default: keys[b] = b (the reference's
+   min-pc rule, pc_vm.py:306-311). Replaces the step selection of pc_vm.step. */
+int ls_machine_set_block_keys(ls_machine* m, const uint32_t* keys, int32_t n_blocks);
 /* same, from device memory (e.g. a torch CUDA tensor) */
 int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes);
 /* Execute up to max_steps steps per group (<0: unbounded). Returns LS_OK and
@@ -235,6 +248,8 @@ int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count);
 /* per-chain block sequences: blocks [z][cap], lens [z] (a len > cap was truncated) */
 int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap);
 int ls_machine_sync(ls_machine* m);
+/* where and how a machine runs: CUDA device, schedule groups, lanes per group */
+int ls_machine_info(const ls_machine* m, int32_t* device, int32_t* groups, int32_t* lanes_per_group);
 int ls_machine_destroy(ls_machine* m);
 
 /* page-locked (and device-mapped) host buffers: ls_read_output into one is a direct

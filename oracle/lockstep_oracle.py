@@ -221,11 +221,13 @@ class OracleResult:
 
 
 def run(compiled, inputs, *, depth: int, types: dict, targets: dict, max_steps: int | None = 1_000_000,
-        lane_traces: bool = False, observer=None) -> OracleResult:
+        lane_traces: bool = False, observer=None, chooser=None) -> OracleResult:
     """Masked-mode pc engine: one min-pc block per step until every lane halts.
 
     `compiled` is a CompiledProgram (flat IR + classes + labels), `types` the
     inferred VType per variable, `targets` maps target name -> TargetDensity.
+    `chooser(tops, depths) -> (block, selected mask)` replaces the min-pc rule
+    (tests of the device's other schedules; per-lane results must not change).
     """
     flat, classes = compiled.flat, compiled.classes
     z = inputs[0].shape[0]
@@ -276,8 +278,11 @@ def run(compiled, inputs, *, depth: int, types: dict, targets: dict, max_steps: 
         active = tops != halt
         if not active.any():
             break
-        b = int(tops[active].min())
-        sel = active & (tops == b)
+        if chooser is None:
+            b = int(tops[active].min())
+            sel = active & (tops == b)
+        else:
+            b, sel = chooser(tops, pc.pointers)
         steps.append((b, int(sel.sum())))
         if lane_blocks is not None:
             for lane in np.flatnonzero(sel):
@@ -328,3 +333,82 @@ def run(compiled, inputs, *, depth: int, types: dict, targets: dict, max_steps: 
         if max_steps is not None and n >= max_steps and (pc.cached_top != halt).any():
             raise StepLimit(max_steps)
     return OracleResult(value(flat.output).copy(), steps, lane_blocks, stack_ops)
+
+
+# ---- the local-static engine (reference local_exec.py:81-185, Alg. 1) -----------------------
+
+
+def run_local(program, inputs, *, targets: dict, max_steps: int | None = 1_000_000):
+    """Masked-mode restatement of `run_local` on a CallGraphProgram.
+
+    One activation of a function runs as a batched frame: every lane holds its
+    own block cursor, each step runs the lowest populated block (min-pc
+    chooser, local_exec.py:44-46) under the lane mask, and a call recurses on
+    the host with the current mask (local_exec.py:81-128). Returns (output,
+    steps) with one (label "fn.block", active lanes, grad invocations) per step.
+    """
+    from paper_1910_11141_b200 import ir  # IR node types only
+
+    z = inputs[0].shape[0]
+    grads = {t.grad for t in targets.values()}
+    steps: list = []
+    kernels: dict = {}
+
+    def kernel(name):
+        k = kernels.get(name)
+        if k is None:
+            k = kernels[name] = kernel_for(name, targets)
+        return k
+
+    def store(env, name, res, mask):
+        dest = env.get(name)
+        if dest is None:
+            dest = env[name] = np.zeros_like(res)
+        dest[mask] = res[mask]
+
+    def call(fidx, args, live):
+        fn = program.functions[fidx]
+        halt = len(fn.blocks)
+        env = {p: np.array(a, copy=True) for p, a in zip(fn.params, args)}
+        pc = np.where(live, 0, halt).astype(np.int64)
+        while True:
+            cand = pc < halt
+            if not cand.any():
+                break
+            b = int(pc[cand].min())
+            sel = cand & (pc == b)
+            if max_steps is not None and len(steps) >= max_steps:
+                raise StepLimit(max_steps)
+            block = fn.blocks[b]
+            g = sum(1 for op in block.ops if isinstance(op, ir.Primitive) and op.prim.name in grads)
+            steps.append((f"{fn.name}.{b}", int(sel.sum()), g))
+            for op in block.ops:
+                if isinstance(op, ir.Primitive):
+                    k = kernel(op.prim.name)
+                    with np.errstate(all="ignore"):
+                        if isinstance(k, tuple):
+                            res = np.full(z, k[1], dtype=np.asarray(k[1]).dtype)
+                        else:
+                            res = k(*(env[a] for a in op.inputs))
+                    store(env, op.output, np.asarray(res), sel)
+                else:
+                    ret = call(op.callee, tuple(env[a] for a in op.args), sel)
+                    store(env, op.output, ret, sel)
+            t = block.terminator
+            if isinstance(t, ir.Jump):
+                pc[sel] = t.target
+            elif isinstance(t, ir.Branch):
+                pc[sel] = np.where(env[t.cond][sel], t.true_target, t.false_target)
+            else:
+                pc[sel] = halt
+        out = env.get(fn.output)
+        return np.zeros(z, dtype=np.int64) if out is None else out
+
+    return call(program.entry, tuple(inputs), np.ones(z, dtype=bool)), steps
+
+
+def utilization(steps, z: int) -> float:
+    """metrics.utilization (reference metrics.py:52-76) over (label, active, grads) steps."""
+    useful = sum(a * g for _, a, g in steps)
+    launched = sum(z * g for _, _, g in steps)
+    return useful / launched

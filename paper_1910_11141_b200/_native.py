@@ -23,7 +23,7 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "lockstep_b200.h"
 
 LS_OK, LS_EINVAL, LS_ECUDA, LS_ENOMEM = 0, -1, -2, -3
 RUN_HALTED, RUN_PAUSED, RUN_OVERFLOW, RUN_UNDERFLOW, RUN_STEP_LIMIT = 0, 1, 2, 3, 4
-SCHED = {"min_pc": 0, "most_populated": 1}
+SCHED = {"min_pc": 0, "most_populated": 1, "local": 2, "priority": 3}
 MF_NO_STAGE = 1  # ls_machine_opts.flags (lockstep_b200.h)
 
 
@@ -56,6 +56,8 @@ _SIGS = {
     "ls_machine_set_output_host": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_last_error": ([], C.c_char_p),
     "ls_device_count": ([C.POINTER(C.c_int32)], C.c_int),
+    "ls_set_device": ([C.c_int32], C.c_int),
+    "ls_machine_info": ([C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
     "ls_program_create": ([C.POINTER(ProgramDesc), C.POINTER(C.c_void_p)], C.c_int),
     "ls_program_bind_target": ([C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_void_p, C.c_double], C.c_int),
@@ -64,6 +66,7 @@ _SIGS = {
                            C.POINTER(C.c_void_p)], C.c_int),
     "ls_machine_set_input": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_machine_reset": ([C.c_void_p], C.c_int),
+    "ls_machine_set_block_keys": ([C.c_void_p, C.c_void_p, C.c_int32], C.c_int),
     "ls_machine_set_input_device": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_run": ([C.c_void_p, C.c_int64, C.POINTER(Status)], C.c_int),
     "ls_read_output": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
@@ -131,10 +134,13 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
 class Program:
     """Owns an `ls_program` built from a DeviceProgram (in library `lib_path`)."""
 
-    def __init__(self, dp: DeviceProgram, lib_path: Path | str | None = None):
+    def __init__(self, dp: DeviceProgram, lib_path: Path | str | None = None, device: int | None = None):
         self.lib = load(lib_path)
         self.lib_path = str(lib_path or LIB_PATH)
         self.dp = dp
+        if device is not None:  # the program (and its machines) live on this CUDA device
+            _check(self.lib.ls_set_device(int(device)), self.lib)
+        self.device = device
         self._keep = [np.ascontiguousarray(dp.blocks), np.ascontiguousarray(dp.ops),
                       np.ascontiguousarray(dp.vars), np.ascontiguousarray(dp.inputs, dtype=np.int32)]
         b, o, v, i = self._keep
@@ -257,6 +263,24 @@ class MachineHandle:
 
     def reset(self) -> None:
         self._c(self.lib.ls_machine_reset(self.handle))
+
+    def info(self) -> tuple[int, int, int]:
+        """(CUDA device, schedule groups, lanes per group)."""
+        d, g, l = C.c_int32(), C.c_int32(), C.c_int32()
+        self._c(self.lib.ls_machine_info(self.handle, C.byref(d), C.byref(g), C.byref(l)))
+        return d.value, g.value, l.value
+
+    @property
+    def groups(self) -> int:
+        return self.info()[1]
+
+    @property
+    def device(self) -> int:
+        return self.info()[0]
+
+    def set_block_keys(self, keys: np.ndarray) -> None:
+        keys = np.ascontiguousarray(keys, dtype=np.uint32)
+        self._c(self.lib.ls_machine_set_block_keys(self.handle, _ptr(keys), len(keys)))
 
     def set_input_device(self, idx: int, dev_ptr: int, nbytes: int) -> None:
         self._c(self.lib.ls_machine_set_input_device(self.handle, idx, C.c_void_p(dev_ptr), nbytes))

@@ -47,6 +47,7 @@ namespace {
 
 struct CtaShared {
   int pick;
+  unsigned pick_key;
   int count;
   unsigned long long fault_key;
   int warp_val[kMaxLanes / 32];
@@ -116,16 +117,19 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
       }
       __syncthreads();
     } else {
-      const int m = __reduce_min_sync(kFull, (unsigned)pc);
-      if (lane_id == 0) sh.warp_val[warp] = m;
+      // keyed rules (min_pc, priority, local): least key over the group's live lanes
+      const unsigned key = pc == a.halt ? 0xffffffffu : lane_key(a, pc, *pc_sp);
+      const unsigned m = __reduce_min_sync(kFull, key);
+      if (lane_id == 0) sh.warp_val[warp] = (int)m;
       __syncthreads();
       if (t == 0) {
-        int mm = a.halt;
-        for (int w2 = 0; w2 < nwarps; ++w2) mm = min(mm, sh.warp_val[w2]);
-        sh.pick = mm;
+        unsigned mm = 0xffffffffu;
+        for (int w2 = 0; w2 < nwarps; ++w2) mm = min(mm, (unsigned)sh.warp_val[w2]);
+        sh.pick = mm == 0xffffffffu ? a.halt : (int)(mm & 0xffffu);
+        sh.pick_key = mm;
       }
       __syncthreads();
-      const unsigned bal = __ballot_sync(kFull, pc == sh.pick && pc != a.halt);
+      const unsigned bal = __ballot_sync(kFull, key == sh.pick_key && pc != a.halt);
       if (lane_id == 0) sh.warp_cnt[warp] = __popc(bal);
       __syncthreads();
       if (t == 0) {
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
       if (t == 0) a.paused[1] = 1;
       break;
     }
-    const bool active = pc == b;
+    const bool active = pc == b && (a.sched == LS_SCHED_MOST_POPULATED || lane_key(a, pc, *pc_sp) == sh.pick_key);
     if (active && a.lane_trace != nullptr) lane_trace_put(a, *my_chain, b);
     StepFault f;
     const bool halted_now = exec_block<false>(a, ln, b, active, *my_chain, f, nullptr);
@@ -158,12 +162,13 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
     if (sh.fault_key != ~0ull) {
       if ((unsigned)(sh.fault_key & 0xffffffffu) == (unsigned)t && f.pos &&
           (unsigned)(f.pos - 1) == (unsigned)(sh.fault_key >> 32)) {
-        a.fault->key = sh.fault_key;
-        a.fault->kind = f.kind;
-        a.fault->var = f.var;
-        a.fault->block = b;
-        a.fault->detail = f.detail;
-        a.fault->chain = *my_chain;
+        FaultRec& fr = a.fault[g];  // one slot per group: the host picks the lowest chain
+        fr.key = sh.fault_key;
+        fr.kind = f.kind;
+        fr.var = f.var;
+        fr.block = b;
+        fr.detail = f.detail;
+        fr.chain = *my_chain;
         __threadfence();
         atomicExch(a.abort_flag, 1);
       }
@@ -221,7 +226,9 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
   long long steps = a.group_steps[g];
   long long* bsteps = a.blk_steps + (size_t)g * a.n_blocks;
   long long* bactive = a.blk_active + (size_t)g * a.n_blocks;
+#if LSB_BLOCK_PROFILE
   long long* bcycles = a.blk_cycles + (size_t)g * a.n_blocks;
+#endif
   unsigned long long useful = 0, launched = 0;
   if (a.group_done[g]) return;
   // the lane's chain id lives in a register; chain_of is updated whenever it changes
@@ -263,7 +270,16 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       const unsigned best = __reduce_max_sync(kFull, key);
       b = best == 0 ? a.halt : (int)(0xffffu - (best & 0xffffu));
     } else {
-      b = (int)__reduce_min_sync(kFull, (unsigned)pc);
+      // keyed rules (min_pc, priority, local): the populated block with the least key;
+      // keys carry the block index in their low 16 bits (host: pc_vm.block_keys)
+#ifdef LSB_GENERATED
+      const int depth_now = psp_r;
+#else
+      const int depth_now = chain >= 0 ? *pc_sp : 0;
+#endif
+      const unsigned key = pc == a.halt ? 0xffffffffu : lane_key(a, pc, depth_now);
+      const unsigned best = __reduce_min_sync(kFull, key);
+      b = best == 0xffffffffu ? a.halt : (int)(best & 0xffffu);
     }
     if (b == a.halt) {
       if (lane == 0) a.group_done[g] = 1;
@@ -275,32 +291,40 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
       if (lane == 0) a.paused[0] = 1;
       break;
     }
-    const bool active = pc == b;
+#ifdef LSB_GENERATED
+    const bool active = pc == b && (a.sched != LS_SCHED_LOCAL || psp_r == __shfl_sync(kFull, psp_r, __ffs(__ballot_sync(kFull, pc == b)) - 1));
+#else
+    const bool active = pc == b && (a.sched != LS_SCHED_LOCAL ||
+                                    *pc_sp == __shfl_sync(kFull, *pc_sp, __ffs(__ballot_sync(kFull, pc == b)) - 1));
+#endif
     const int count = __popc(__ballot_sync(kFull, active));
     if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, b);
     StepFault f;
+#if LSB_BLOCK_PROFILE
     const long long t_start = clock64();
+#endif
 #ifdef LSB_GENERATED
     const bool halted_now = lsbgen::gen_exec_block(a, ln, b, active, chain, f, my_smem, pc_r, psp_r);
 #else
     const bool halted_now = LSB_WARP_EXEC(a, ln, b, active, chain, f, my_smem);
 #endif
     // per-block statistics as fire-and-forget reductions (no read-modify-write stall)
+#if LSB_BLOCK_PROFILE
     if (lane == 0) atomicAdd((unsigned long long*)&bcycles[b], (unsigned long long)(clock64() - t_start));
+#endif
     const unsigned fkey = f.pos ? ((unsigned)(f.pos - 1) << 5) | (unsigned)lane : ~0u;
     const unsigned wmin = __reduce_min_sync(kFull, fkey);
     if (wmin != ~0u) {
       if (fkey == wmin) {
-        // several groups may fault in one launch: the lowest chain is reported
-        const unsigned long long key = (unsigned long long)chain;
-        const unsigned long long old = atomicMin(&a.fault->key, key);
-        if (key < old) {
-          a.fault->kind = f.kind;
-          a.fault->var = f.var;
-          a.fault->block = b;
-          a.fault->detail = f.detail;
-          a.fault->chain = chain;
-        }
+        // several groups may fault in one launch: each writes its own slot (no race) and
+        // the host reports the lowest chain
+        FaultRec& fr = a.fault[g];
+        fr.key = (unsigned long long)chain;
+        fr.kind = f.kind;
+        fr.var = f.var;
+        fr.block = b;
+        fr.detail = f.detail;
+        fr.chain = chain;
         __threadfence();
         atomicExch(a.abort_flag, 1);
       }
@@ -402,6 +426,7 @@ static int upload(T** d, const std::vector<T>& h) {
 }
 
 struct ls_program {
+  int device = 0;
   std::vector<ls_block> blocks;
   std::vector<ls_op> ops;
   std::vector<ls_var> vars;
@@ -415,6 +440,7 @@ struct ls_program {
 
 struct ls_machine {
   ls_program* p = nullptr;
+  int device = 0;
   long long z = 0;
   int depth = 0, lanes = 0, groups = 0, group_rows = 0;
   ls_machine_opts opts{};
@@ -444,6 +470,7 @@ struct ls_machine {
   long long* blk_active = nullptr;
   long long* blk_cycles = nullptr;
   FaultRec* fault = nullptr;
+  unsigned* bkey = nullptr;  // [n_blocks] schedule keys
   int* flags = nullptr;  // [0] abort [1] paused-steps [2] paused-trace
   int* lane_trace = nullptr;
   int* lane_trace_len = nullptr;
@@ -542,6 +569,7 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   a.stage_src = m->stage_target >= 0 ? p->targets[m->stage_target].B1 : nullptr;
   a.lane_trace = m->lane_trace; a.lane_trace_len = m->lane_trace_len; a.lane_trace_cap = m->lane_trace_cap;
   a.fault = m->fault; a.abort_flag = m->flags + 0; a.paused = m->flags + 1;
+  a.bkey = m->bkey;
   return a;
 }
 
@@ -563,9 +591,29 @@ int ls_device_count(int32_t* n) {
   return LS_OK;
 }
 
+int ls_set_device(int32_t device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    return fail(LS_ECUDA, "ls_set_device: no such CUDA device");
+  }
+  CK(cudaSetDevice(device));
+  return LS_OK;
+}
+
+int ls_machine_info(const ls_machine* m, int32_t* device, int32_t* groups, int32_t* lanes_per_group) {
+  if (!m) return fail(LS_EINVAL, "null machine");
+  if (device) *device = m->device;
+  if (groups) *groups = m->groups;
+  if (lanes_per_group) *lanes_per_group = m->lanes;
+  return LS_OK;
+}
+
 int ls_program_create(const ls_program_desc* d, ls_program** out) {
   if (!d || !out || d->n_blocks < 1 || d->n_vars < 1) return fail(LS_EINVAL, "empty program");
   auto* p = new ls_program();
+  cudaGetDevice(&p->device);
+  cudaGetLastError();
   p->blocks.assign(d->blocks, d->blocks + d->n_blocks);
   p->ops.assign(d->ops, d->ops + d->n_ops);
   p->vars.assign(d->vars, d->vars + d->n_vars);
@@ -588,6 +636,7 @@ int ls_program_create(const ls_program_desc* d, ls_program** out) {
 int ls_program_bind_target(ls_program* p, int32_t slot, int32_t kind, int32_t dim, int32_t n,
                            const double* params, double norm) {
   if (!p || slot < 0 || slot >= kMaxTargets || dim < 1) return fail(LS_EINVAL, "bad target slot");
+  CK(cudaSetDevice(p->device));
   const int rows = kind == LS_TARGET_GAUSSIAN ? dim : n;
   if (rows < 1) return fail(LS_EINVAL, "bad target shape");
   std::vector<double> h(params, params + (size_t)rows * dim), ht((size_t)rows * dim);
@@ -630,6 +679,7 @@ int ls_program_bind_target(ls_program* p, int32_t slot, int32_t kind, int32_t di
 
 int ls_program_destroy(ls_program* p) {
   if (!p) return LS_OK;
+  cudaSetDevice(p->device);
   for (double* q : p->owned) cudaFree(q);
   delete p;
   return LS_OK;
@@ -637,6 +687,7 @@ int ls_program_destroy(ls_program* p) {
 
 int ls_machine_destroy(ls_machine* m) {
   if (!m) return LS_OK;
+  cudaSetDevice(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   cudaFree(m->d_blocks); cudaFree(m->d_ops); cudaFree(m->d_input_width); cudaFree(m->d_input_rows);
   cudaFree(m->ws); cudaFree(m->sp); cudaFree(m->pcs); cudaFree(m->chain_of);
@@ -645,7 +696,7 @@ int ls_machine_destroy(ls_machine* m) {
   cudaFree(m->group_steps); cudaFree(m->group_done); cudaFree(m->trace_block);
   cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
   cudaFree(m->blk_active); cudaFree(m->blk_cycles); cudaFree(m->fault); cudaFree(m->flags);
-  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len);
+  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len); cudaFree(m->bkey);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -667,8 +718,12 @@ static int reset_state(ls_machine* m) {
   CK(cudaMemsetAsync(m->flags, 0, 4 * sizeof(int), m->stream));
   CK(cudaMemsetAsync(m->trace_n, 0, sizeof(long long), m->stream));
   if (m->lane_trace_len) CK(cudaMemsetAsync(m->lane_trace_len, 0, (size_t)m->z * sizeof(int), m->stream));
-  FaultRec f0{~0ull, 0, 0, 0, 0, -1};
-  CK(cudaMemcpyAsync(m->fault, &f0, sizeof(f0), cudaMemcpyHostToDevice, m->stream));
+  {
+    const FaultRec f0{~0ull, 0, 0, 0, 0, -1};
+    std::vector<FaultRec> fr((size_t)m->groups, f0);
+    CK(cudaMemcpyAsync(m->fault, fr.data(), fr.size() * sizeof(FaultRec), cudaMemcpyHostToDevice, m->stream));
+    CK(cudaStreamSynchronize(m->stream));
+  }
   std::vector<long long> slots((size_t)m->groups * L, -1);
   if (!m->refill)
     for (size_t t = 0; t < L; ++t) slots[t] = (long long)t < m->z ? (long long)t : -2;
@@ -687,13 +742,14 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     cudaGetLastError();
     return fail(LS_ECUDA, "no CUDA device: the lockstep B200 engine has no CPU fallback");
   }
+  CK(cudaSetDevice(p->device));  // a machine lives on its program's device
   auto* m = new ls_machine();
   m->p = p;
+  m->device = p->device;
   m->z = z;
   m->depth = depth;
   if (opts) m->opts = *opts;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
+  int dev = p->device, sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int groups;
   m->warp = m->opts.warp_groups != 0;
@@ -824,9 +880,17 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       (rc = dalloc(&m->blk_steps, (size_t)groups * p->blocks.size())) ||
       (rc = dalloc(&m->blk_active, (size_t)groups * p->blocks.size())) ||
       (rc = dalloc(&m->blk_cycles, (size_t)groups * p->blocks.size())) ||
-      (rc = dalloc(&m->fault, 1)) || (rc = dalloc(&m->flags, 4)) || (rc = dalloc(&m->trace_n, 1))) {
+      (rc = dalloc(&m->fault, (size_t)groups)) || (rc = dalloc(&m->flags, 4)) || (rc = dalloc(&m->trace_n, 1))) {
     ls_machine_destroy(m);
     return rc;
+  }
+  {
+    std::vector<unsigned> keys(p->blocks.size());
+    for (size_t b = 0; b < keys.size(); ++b) keys[b] = (unsigned)b;  // reference min-pc
+    if ((rc = upload(&m->bkey, keys))) {
+      ls_machine_destroy(m);
+      return rc;
+    }
   }
   for (size_t k = 0; k < p->inputs.size(); ++k) {
     uint64_t* buf = nullptr;
@@ -864,13 +928,25 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   return LS_OK;
 }
 
+int ls_machine_set_block_keys(ls_machine* m, const uint32_t* keys, int32_t n_blocks) {
+  if (!m || !keys || n_blocks != (int32_t)m->p->blocks.size()) return fail(LS_EINVAL, "bad block keys");
+  CK(cudaSetDevice(m->device));
+  for (int b = 0; b < n_blocks; ++b)
+    if ((int)(keys[b] & 0xffffu) != b || keys[b] == 0xffffffffu)
+      return fail(LS_EINVAL, "block key must carry its block index in bits 0..15");
+  CK(cudaMemcpy(m->bkey, keys, (size_t)n_blocks * sizeof(unsigned), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
 int ls_machine_reset(ls_machine* m) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   return reset_state(m);
 }
 
 int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t bytes) {
   if (!m || idx < 0 || idx >= (int)m->inputs.size()) return fail(LS_EINVAL, "bad input index");
+  CK(cudaSetDevice(m->device));
   if (bytes != m->z * m->input_width[idx] * 8) return fail(LS_EINVAL, "input size mismatch");
   CK(cudaMemcpyAsync(m->inputs[idx], host, bytes, cudaMemcpyHostToDevice, m->stream));
   CK(cudaStreamSynchronize(m->stream));
@@ -879,6 +955,7 @@ int ls_machine_set_input(ls_machine* m, int32_t idx, const void* host, int64_t b
 
 int ls_machine_set_input_device(ls_machine* m, int32_t idx, const void* dev, int64_t bytes) {
   if (!m || idx < 0 || idx >= (int)m->inputs.size()) return fail(LS_EINVAL, "bad input index");
+  CK(cudaSetDevice(m->device));
   if (bytes != m->z * m->input_width[idx] * 8) return fail(LS_EINVAL, "input size mismatch");
   CK(cudaMemcpyAsync(m->inputs[idx], dev, bytes, cudaMemcpyDeviceToDevice, m->stream));
   return static_init(m);
@@ -902,6 +979,7 @@ extern "C" {
 
 int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   if (!m || !st) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   ls_program* p = m->p;
   VMArgs a = make_args(m, max_steps);
   m->started = true;
@@ -932,7 +1010,13 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   std::vector<int> gdone(m->groups);
   unsigned long long cnt[3];
   CK(cudaMemcpy(flags, m->flags, sizeof(flags), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(&f, m->fault, sizeof(f), cudaMemcpyDeviceToHost));
+  {
+    std::vector<FaultRec> fr((size_t)m->groups);
+    CK(cudaMemcpy(fr.data(), m->fault, fr.size() * sizeof(FaultRec), cudaMemcpyDeviceToHost));
+    f = fr[0];
+    for (const auto& x : fr)  // the lowest chain among the groups that faulted
+      if (x.chain >= 0 && (f.chain < 0 || x.chain < f.chain)) f = x;
+  }
   CK(cudaMemcpy(gsteps.data(), m->group_steps, m->groups * sizeof(long long), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(gdone.data(), m->group_done, m->groups * sizeof(int), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cnt, m->counters, sizeof(cnt), cudaMemcpyDeviceToHost));
@@ -961,6 +1045,7 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
 
 int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
   if (m->out_host_dev) {  // the kernel wrote the rows straight into the host buffer
     CK(cudaStreamSynchronize(m->stream));
@@ -974,6 +1059,7 @@ int ls_read_output(ls_machine* m, void* host, int64_t bytes) {
 
 int ls_machine_set_output_host(ls_machine* m, void* host, int64_t bytes) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   if (!host) {
     m->out_host = nullptr;
     m->out_host_dev = nullptr;
@@ -1009,6 +1095,7 @@ int ls_host_free(void* host) {
 
 int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
   if (!m || !dev_dst) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
   CK(cudaMemcpyAsync(dev_dst, m->out_host_dev ? m->out_host_dev : m->output, bytes, cudaMemcpyDefault,
                      m->stream));
@@ -1018,12 +1105,14 @@ int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
 
 int ls_output_device(ls_machine* m, void** dev) {
   if (!m || !dev) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   *dev = m->out_host_dev ? m->out_host_dev : m->output;
   return LS_OK;
 }
 
 int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap, int64_t* n) {
   if (!m || !n) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   *n = 0;
   if (!m->trace_block) return LS_OK;
   long long have = 0;
@@ -1048,6 +1137,7 @@ int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap,
 
 int ls_block_totals(ls_machine* m, int64_t* steps, int64_t* active) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   const size_t nb = m->p->blocks.size();
   std::vector<long long> s((size_t)m->groups * nb), a((size_t)m->groups * nb);
   CK(cudaMemcpy(s.data(), m->blk_steps, s.size() * sizeof(long long), cudaMemcpyDeviceToHost));
@@ -1077,6 +1167,7 @@ int ls_debug_sb_profile(uint64_t* out8) {
 
 int ls_block_cycles(ls_machine* m, int64_t* cycles) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   const size_t nb = m->p->blocks.size();
   std::vector<long long> c((size_t)m->groups * nb);
   CK(cudaMemcpy(c.data(), m->blk_cycles, c.size() * sizeof(long long), cudaMemcpyDeviceToHost));
@@ -1090,6 +1181,7 @@ int ls_block_cycles(ls_machine* m, int64_t* cycles) {
 
 int ls_read_var(ls_machine* m, int32_t var, void* host, int64_t bytes) {
   if (!m || var < 0 || var >= (int)m->p->vars.size()) return fail(LS_EINVAL, "bad var");
+  CK(cudaSetDevice(m->device));
   if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
   const int slots = m->var_depth[var], w = m->p->vars[var].width;
   const long long z = m->z;
@@ -1105,6 +1197,7 @@ int ls_read_var(ls_machine* m, int32_t var, void* host, int64_t bytes) {
 
 int ls_read_pointers(ls_machine* m, int32_t var, int64_t* host, int64_t z) {
   if (!m || z != m->z) return fail(LS_EINVAL, "bad pointer request");
+  CK(cudaSetDevice(m->device));
   if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
   int row;
   if (var < 0) row = m->p->n_stacked;
@@ -1118,6 +1211,7 @@ int ls_read_pointers(ls_machine* m, int32_t var, int64_t* host, int64_t z) {
 
 int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count) {
   if (!m || count != (int64_t)(m->depth + 1) * m->z) return fail(LS_EINVAL, "bad pc request");
+  CK(cudaSetDevice(m->device));
   if (m->groups != 1 || m->refill) return fail(LS_EINVAL, "observer access needs a single schedule group");
   std::vector<int> raw((size_t)(m->depth + 1) * m->lanes);
   CK(cudaMemcpy(raw.data(), m->pcs, raw.size() * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1128,6 +1222,7 @@ int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count) {
 
 int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap) {
   if (!m || !m->lane_trace) return fail(LS_EINVAL, "machine was created without lane traces");
+  CK(cudaSetDevice(m->device));
   if (cap != m->lane_trace_cap) return fail(LS_EINVAL, "lane trace capacity mismatch");
   CK(cudaMemcpy(blocks, m->lane_trace, (size_t)m->z * cap * sizeof(int), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(lens, m->lane_trace_len, (size_t)m->z * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1136,6 +1231,7 @@ int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t c
 
 int ls_machine_sync(ls_machine* m) {
   if (!m) return fail(LS_EINVAL, "null machine");
+  CK(cudaSetDevice(m->device));
   CK(cudaStreamSynchronize(m->stream));
   return LS_OK;
 }

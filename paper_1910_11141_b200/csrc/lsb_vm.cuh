@@ -114,10 +114,21 @@ struct VMArgs {
   int* lane_trace;
   int* lane_trace_len;
   int lane_trace_cap;
-  FaultRec* fault;
+  FaultRec* fault;              // [n_groups] one fault slot per group
   int* abort_flag;
   int* paused;
+  const unsigned* bkey;         // [n_blocks] schedule key of each block (block index in bits 0..15)
 };
+
+// Schedule key of a live lane at block `pc` with pc-stack depth `psp` (keyed rules pick the
+// least): min_pc keys are the block index; priority keys rank blocks (host: pc_vm.block_keys);
+// the local rule (paper Alg. 1, reference local_exec.py) runs the deepest activation first.
+__device__ __forceinline__ unsigned lane_key(const VMArgs& a, int pc, int psp) {
+  const unsigned k = __ldg(&a.bkey[pc]);
+  if (a.sched != LS_SCHED_LOCAL) return k;
+  const unsigned d = psp < 0 ? 0u : (psp > 255 ? 255u : (unsigned)psp);
+  return ((255u - d) << 24) | (k & 0x00ffffffu);
+}
 
 struct Lane {
   uint64_t* ws;  // group workspace

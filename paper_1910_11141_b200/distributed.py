@@ -62,10 +62,10 @@ def _stats(chains, max_lag: int):
     halves = torch.cat([chains[:, :h], chains[:, n - h:]], dim=0)  # [2c, h, d]
     means = halves.mean(dim=1)
     var = halves.var(dim=1, unbiased=True)
-    centered = chains - chains.mean(dim=1, keepdim=True)
+    centered = halves - means[:, None, :]
     acov = []
-    for lag in range(max_lag + 1):
-        prod = (centered[:, : n - lag] * centered[:, lag:]).sum(dim=1) / n  # [c, d]
+    for lag in range(max_lag + 1):  # biased autocovariance of each half-chain (divided by h)
+        prod = (centered[:, : h - lag] * centered[:, lag:]).sum(dim=1) / h  # [2c, d]
         acov.append(prod.sum(dim=0))
     parts = [torch.tensor([2.0 * c], dtype=torch.float64, device=chains.device), means.sum(0),
              (means ** 2).sum(0), var.sum(0), chains.sum((0, 1)), (chains ** 2).sum((0, 1)),
@@ -83,7 +83,7 @@ def diagnostics(chains, *, group=None, max_lag: int = 50) -> Diagnostics:
     import torch.distributed as dist
 
     c, n, d = chains.shape
-    max_lag = min(max_lag, n - 1)
+    max_lag = min(max_lag, n // 2 - 1)
     s = _stats(chains.to(torch.float64), max_lag)
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(s, group=group)
@@ -103,16 +103,20 @@ def diagnostics(chains, *, group=None, max_lag: int = 50) -> Diagnostics:
     draws_total = chains_total * n
     mean = sum_x / draws_total
     var = sum_x2 / draws_total - mean ** 2
-    # ESS from the chain-averaged autocorrelation (Geyer initial positive sequence)
-    rho = acov / chains_total / np.maximum(acov[0] / chains_total, 1e-300)
+    # ESS (Stan / Geyer): rho_t = 1 - (W - mean half-chain autocovariance_t) / var_plus, then
+    # the initial positive sequence of pair sums P_k = rho_2k + rho_2k+1 (k = 0, 1, ...), made
+    # monotone, tau = -1 + 2 sum P_k; antithetic chains (rho_1 < 0) may give ESS > draws
+    rho = 1.0 - (w[None, :] - acov / m2) / np.maximum(var_plus[None, :], 1e-300)
     ess = np.empty(d)
     for j in range(d):
-        tau = 1.0
-        for k in range(1, max_lag, 2):
-            pair = rho[k, j] + (rho[k + 1, j] if k + 1 <= max_lag else 0.0)
-            if pair <= 0:
+        total, prev = 0.0, np.inf
+        for k in range(0, max_lag, 2):
+            pair = rho[k, j] + rho[k + 1, j]
+            if pair < 0:
                 break
-            tau += 2 * pair
+            prev = min(prev, pair)
+            total += prev
+        tau = max(-1.0 + 2.0 * total, 1.0 / np.log10(max(draws_total, 10.0)))
         ess[j] = draws_total / tau
     return Diagnostics(rhat=rhat, ess=ess, mean=mean, var=var, chains=int(chains_total), draws=n)
 

@@ -608,7 +608,9 @@ def superblock_io(flat: ir.FlatProgram, m: dict) -> tuple[dict, set[tuple[int, i
                if isinstance(blk.terminator, ir.PushJump) and blk.terminator.jump_to == m["entry"]]
     fwd, drop = {}, set()
     for param in (m["q"], m["p"]):
-        if read_outside(param) or not callers:
+        # the program's entry function is also entered without a call: its parameters are
+        # the inputs, never a caller's argument sources
+        if read_outside(param) or not callers or m["entry"] == flat.entry:
             continue
         srcs, pos = set(), set()
         for cb in callers:

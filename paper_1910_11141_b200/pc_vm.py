@@ -31,6 +31,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native, ir
+from . import schedule as _schedule
 from .compiler import CompiledProgram
 from .errors import (StackFault, StackOverflow, StackUnderflow, StepLimitExceeded,
                      TypeInferenceError)
@@ -301,7 +302,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
                  lanes_per_group: int | None = None, groups: int = 0,
                  optimize: bool = False, exact_logpdf: bool = True,
                  lane_trace_cap: int = 0, engine: str = "auto",
-                 codegen: bool | str = False, reuse: bool = False) -> Machine:
+                 codegen: bool | str = False, reuse: bool = False, device: int | None = None) -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
@@ -316,6 +317,11 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     codegen (warp engine): run program-specialised block code (codegen.py)
     instead of the op interpreter; compiled once per program and cached
     in-tree ("cached": use only a prebuilt library).
+
+    device: CUDA device index the machine lives on (one process per GPU passes
+    its LOCAL_RANK; None = the library's current device, 0 by default).
+    schedule: block-selection rule (schedule.SCHEDULES): "min_pc" (reference),
+    "most_populated", "local" (paper Alg. 1) or "priority" (throughput).
     """
     if mode not in ("masked", "gather"):
         raise ValueError(f"unknown mode '{mode}'")
@@ -332,7 +338,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     if kind == "exact" and z > MAX_GROUP_LANES:
         raise ValueError(f"the exact engine holds at most {MAX_GROUP_LANES} lanes")
     pkey = (id(compiled), tuple(map(str, in_types)), optimize, kind == "warp",
-            codegen if kind == "warp" else False)
+            codegen if kind == "warp" else False, device)
     hit = _PROGRAM_CACHE.get(pkey)
     if hit is not None and hit[0] is compiled:
         dp, program, types = hit[1], hit[2], hit[3]
@@ -346,7 +352,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
             lib = _cg.library_for(dp, build=codegen != "cached")
             if lib is None:
                 raise ValueError("no prebuilt specialised library for this program (codegen='cached')")
-        program = _native.Program(dp, lib)
+        program = _native.Program(dp, lib, device=device)
         if len(_PROGRAM_CACHE) >= 16:
             _PROGRAM_CACHE.pop(next(iter(_PROGRAM_CACHE)))
         _PROGRAM_CACHE[pkey] = (compiled, dp, program, types)
@@ -365,10 +371,14 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
         handle = _native.MachineHandle(program, z, depth, **mopts)
     if reuse:  # run() hands the machine back to the cache when it is done with it
         handle.cache_key = mkey
+    keys = _schedule.block_keys(flat, compiled.labels, schedule,
+                                np.flatnonzero(np.asarray(dp.blocks["grads"]) > 0))
+    handle.set_block_keys(keys)
     for k, a in enumerate(arrays):
         handle.set_input(k, _as_words(a))
     m = Machine(compiled, dp, handle, z, depth, mode, types, trace, schedule, exact, lanes)
     m.engine = kind
+    m._keys = keys
     if not exact and trace is not None:
         m.trace = GroupTrace("pc", z, compiled.labels, dp.block_prims, lanes,
                              np.zeros(len(flat.blocks), np.int64), np.zeros(len(flat.blocks), np.int64))
@@ -416,17 +426,13 @@ def _absorb(m: Machine, st) -> None:
 def step(m: Machine, *, observer=None, debug: bool = False) -> bool:
     """Execute one batched block on the device; False once every lane has halted."""
     m._need_exact()
-    tops = m.pc_tops()
+    pc = m.pc
+    tops = pc.cached_top
     active = tops != m.halt_index
     if not active.any():
         m.halted = True
         return False
-    if m.schedule == "min_pc":
-        b = int(tops[active].min())
-    else:
-        vals, counts = np.unique(tops[active], return_counts=True)
-        b = int(vals[np.argmax(counts)])
-    sel = active & (tops == b)
+    b, sel = _schedule.select(m.schedule, tops, pc.pointers, m._keys, m.halt_index)
     st = m._h.run(m.steps + 1)
     if st.kind in (_native.RUN_OVERFLOW, _native.RUN_UNDERFLOW):
         _absorb(m, st)
@@ -482,7 +488,8 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
         max_steps: int | None = DEFAULT_MAX_STEPS, observer=None, debug: bool = False,
         schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
         optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
-        engine: str = "auto", codegen: bool | str = False, return_machine: bool = False):
+        engine: str = "auto", codegen: bool | str = False, return_machine: bool = False,
+        device: int | None = None):
     """Execute a compiled program on the B200; returns (outputs, trace)."""
     arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
     z = arrays[0].shape[0] if arrays else 0
@@ -495,9 +502,10 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
                      exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
-                     codegen=codegen, reuse=reuse)
-    if m.engine == "warp" and observer is None and not debug:
-        # output rows go straight to a pinned host buffer while the run executes
+                     codegen=codegen, reuse=reuse, device=device)
+    if m.engine == "warp" and observer is None and not debug and not return_machine:
+        # output rows go straight to a pinned host buffer while the run executes (not for
+        # a machine handed back: its device output must stay valid for later reads)
         m._h.stream_output_to_host(m._dp.types[m.flat.output].words)
     try:
         out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)

@@ -15,13 +15,13 @@ from .runtime import VType
 F64, I64 = VType("f64"), VType("i64")
 
 
-def nuts(dim: int, rho: float, **cfg):
+def nuts(dim: int, rho: float, entry: str = "nuts_main", **cfg):
     from . import compile_program, compile_source, correlated_gaussian, nuts_lite_source
     from .workloads import NutsConfig
 
     config = NutsConfig(**cfg)
     target = correlated_gaussian(dim, rho)
-    cp = compile_program(compile_source(nuts_lite_source(config, target), "nuts_main"))
+    cp = compile_program(compile_source(nuts_lite_source(config, target), entry))
     return config, target, cp
 
 
@@ -32,6 +32,9 @@ TEST_NUTS = [
     dict(dim=100, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=10, iterations=3),
     dict(dim=5, rho=0.5, step_size=0.25, leaf_steps=4, max_depth=8, iterations=4),
 ]
+# single-leaf programs (entry = leapfrog) whose fused superblock the per-step test checks
+# against the reference's leapfrog vectors (tests/golden/leapfrog.npz)
+LEAPFROG = [(2, 1), (2, 4), (100, 1), (100, 4)]
 # logistic-regression cases (DMMA two-GEMM gradient): gradient-only programs and one NUTS run
 LR_GRAD = [(200, 5, 7), (1000, 25, 0)]
 LR_NUTS = dict(n=200, d=5, seed=7, step_size=0.1, leaf_steps=2, max_depth=5, iterations=3)
@@ -64,6 +67,9 @@ def specs():
         dim, rho = kw.pop("dim"), kw.pop("rho")
         _, _, cp = nuts(dim, rho, **kw)
         out.append((f"nuts_d{dim}_T{kw['iterations']}", cp, [VType("f64", dim), I64]))
+    for d, steps in LEAPFROG:
+        _, _, cp = nuts(d, 0.5, step_size=0.25, leaf_steps=steps, max_depth=6, iterations=1, entry="leapfrog")
+        out.append((f"leapfrog_d{d}_L{steps}", cp, [VType("f64", d), VType("f64", d), VType("f64")]))
     for n, d, seed in LR_GRAD:
         _, cp = lr_gradient(n, d, seed)
         out.append((f"lr_grad_{n}x{d}", cp, [VType("f64", d)]))

@@ -11,6 +11,7 @@ only) and records, with the numpy/OpenBLAS build of this container:
 * NUTS chains, global traces and per-lane block sequences
 * single-leaf leapfrog vectors (entry='leapfrog')         (test_acceptance.py:294-312)
 * logistic-regression logpdf/grad values                  (workloads.py:216-228)
+* local-static engine schedules + gradient utilisation     (local_exec.py:142-193)
 
 The GPU box has no /root/reference; tests read only these files.
 Usage: python tests/golden/make_golden.py
@@ -38,6 +39,17 @@ NUTS_CASES = [
     ("nuts_d5", 5, 0.5, dict(step_size=0.25, leaf_steps=4, max_depth=10, iterations=5), 32, 1),
     ("nuts_d100", 100, 0.5, dict(step_size=0.25, leaf_steps=4, max_depth=10, iterations=3), 16, 0),
     ("nuts_d3m", 3, -0.2, dict(step_size=0.125, leaf_steps=3, max_depth=8, iterations=6), 24, 7),
+    # the benchmarked configuration (bench.py / prebuilt.BENCH): 100-d, T=10, depth 10
+    ("nuts_d100_T10", 100, 0.5, dict(step_size=0.25, leaf_steps=4, max_depth=10, iterations=10), 64, 0),
+]
+
+# local-static engine (Alg. 1, reference local_exec.py) vs the pc VM: gradient utilisation
+# (reference test_acceptance.py:236-266 runs the first two)
+LOCAL_CASES = [
+    # name, dim, rho, NutsConfig kwargs, z, key seed
+    ("util_z30", 2, 0.5, dict(step_size=0.25, leaf_steps=4, max_depth=6, iterations=12, seed=0), 30, 3),
+    ("util_z1", 2, 0.5, dict(step_size=0.25, leaf_steps=4, max_depth=6, iterations=12, seed=0), 1, 3),
+    ("util_d5_z64", 5, 0.5, dict(step_size=0.1, leaf_steps=4, max_depth=8, iterations=6, seed=0), 64, 11),
 ]
 
 
@@ -149,6 +161,37 @@ def nuts_runs() -> tuple[dict, dict]:
     return arrays, meta
 
 
+def local_runs() -> tuple[dict, dict]:
+    """trace_local (reference local_exec.py:188-193) and pc_vm.run on the same batch: the
+    local engine's schedule, outputs and both gradient utilisations (metrics.py:52-76)."""
+    from lockstep.local_exec import trace_local
+    from lockstep.metrics import utilization
+
+    arrays, meta = {}, {}
+    for name, d, rho, kw, z, seed in LOCAL_CASES:
+        t = R.correlated_gaussian(d, rho)
+        cfg = R.NutsConfig(**kw)
+        src = R.nuts_lite_source(cfg, t)
+        cg = R.compile_source(src, "nuts_main")
+        cp = R.compile_program(cg)
+        q0 = np.zeros((z, d))
+        key = np.random.default_rng(seed).integers(0, 2**31, size=z).astype(np.int64)
+        lout, lt = trace_local(cg, [q0, key])
+        pout, pt = R.pc_vm.run(cp, [q0, key], depth=cfg.min_stack_depth)
+        counted = {t.grad}
+        arrays[f"{name}_key"] = key
+        arrays[f"{name}_local_out"] = lout
+        arrays[f"{name}_pc_out"] = pout
+        labels = sorted({s.block for s in lt.steps})
+        arrays[f"{name}_local_steps"] = np.array(
+            [[labels.index(s.block), s.active, s.prims.get(t.grad, 0)] for s in lt.steps], np.int32)
+        meta[name] = {"dim": d, "rho": rho, "config": kw, "z": z, "key_seed": seed, "target": t.name,
+                      "local_labels": labels,
+                      "util_local": utilization(lt, counted), "util_pc": utilization(pt, counted),
+                      "pc_step_count": pt.step_count, "local_step_count": lt.step_count}
+    return arrays, meta
+
+
 def Rir_index(cp, label: str) -> int:
     return cp.labels.index(label)
 
@@ -194,6 +237,9 @@ def main():
     arrays, nmeta = nuts_runs()
     np.savez_compressed(OUT / "nuts_runs.npz", **arrays)
     meta["nuts"] = nmeta
+    arrays, lmeta = local_runs()
+    np.savez_compressed(OUT / "local_runs.npz", **arrays)
+    meta["local"] = lmeta
     np.savez_compressed(OUT / "leapfrog.npz", **leapfrog_vectors())
     np.savez_compressed(OUT / "logreg.npz", **logreg_values())
     (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")

@@ -23,12 +23,12 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _synthetic_chains(z=64, n=200, d=3, seed=0):
+def _synthetic_chains(z=64, n=200, d=3, seed=0, phi=0.6):
     rng = np.random.default_rng(seed)
     x = np.zeros((z, n, d))
     x[:, 0] = rng.normal(size=(z, d))
-    for t in range(1, n):  # AR(1) chains: known positive autocorrelation
-        x[:, t] = 0.6 * x[:, t - 1] + 0.8 * rng.normal(size=(z, d))
+    for t in range(1, n):  # AR(1) chains: known autocorrelation phi^lag, unit variance
+        x[:, t] = phi * x[:, t - 1] + np.sqrt(1 - phi * phi) * rng.normal(size=(z, d))
     return x
 
 
@@ -87,3 +87,16 @@ def test_diagnostics_behave():
     bad = x.copy()
     bad[:16] += 3.0  # chains stuck in two modes
     assert np.all(D.diagnostics(torch.from_numpy(bad)).rhat > 1.5)
+
+
+@pytest.mark.parametrize("phi", [0.9, 0.6, 0.0, -0.5])
+def test_ess_matches_ar1_theory(phi):
+    """Stan/Geyer ESS against the AR(1) closed form N (1 - phi) / (1 + phi): within 12 %,
+    including antithetic chains (phi < 0), whose ESS exceeds the number of draws."""
+    z, n = 64, 2000
+    x = _synthetic_chains(z=z, n=n, d=2, seed=7, phi=phi)
+    ess = D.diagnostics(torch.from_numpy(x), max_lag=200).ess
+    want = z * n * (1 - phi) / (1 + phi)
+    assert np.all(np.abs(ess / want - 1) < 0.12), (phi, ess, want)
+    if phi < 0:
+        assert np.all(ess > z * n)

@@ -458,3 +458,118 @@ def test_illconditioned_1000d_depth15_lanes_exact(illcond_programs, eps, engine)
     assert np.isfinite(got).all()
     assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
     assert m.useful_grads == tr.useful_invocations({t.grad}) > 0
+
+
+# ---- round 2: the benchmarked library, the superblock per step, device dot, refill, schedules --
+
+
+@pytest.mark.parametrize("schedule", ["min_pc", "priority"])
+def test_bench_library_lanes_exact_against_reference(golden_meta, schedule):
+    """The exact program bench.py times (prebuilt.BENCH: d=100, T=10, depth 10, warp engine,
+    specialised library, fast logpdf): every lane's pc trace equals the reference's own
+    (observer-recorded, tests/golden nuts_d100_T10) and the chains agree with the reference's
+    output; gradient counts are the reference's."""
+    from paper_1910_11141_b200 import prebuilt
+
+    meta = golden_meta["nuts"]["nuts_d100_T10"]
+    g = load_npz("nuts_runs.npz")
+    kw = dict(prebuilt.BENCH)
+    assert {k: meta["config"][k] for k in meta["config"]} == {k: kw[k] for k in meta["config"]}
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+    z = meta["z"]
+    ins = [np.zeros((z, t.dim)), g["nuts_d100_T10_key"]]
+    got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen="cached",
+                       exact_logpdf=False, schedule=schedule, lane_trace_cap=1 << 16, return_machine=True)
+    assert m._h.program.lib_path.endswith(".so") and "/gen/" in m._h.program.lib_path
+    want_lanes = split_lanes(g["nuts_d100_T10_lane_len"], g["nuts_d100_T10_lane_blocks"])
+    for lane, seq in enumerate(m.lane_traces()):
+        assert np.array_equal(seq, want_lanes[lane]), lane
+    want = g["nuts_d100_T10_out"]
+    assert (np.abs(got - want) / np.maximum(np.abs(want), 1.0)).max() < CHAIN_RTOL
+    assert m.useful_grads == meta["useful_grads"]
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_leapfrog_superblock_per_step_tolerance(codegen):
+    """Single leaves through the warp engine's fused DMMA leapfrog superblock (the headline's
+    gradient path) against the reference's vectors: 1e-12 relative per leapfrog step, scaled
+    by each lane's largest component (reference gradient: OpenBLAS dgemm)."""
+    from paper_1910_11141_b200 import prebuilt
+
+    g = load_npz("leapfrog.npz")
+    for d, steps in prebuilt.LEAPFROG:
+        _, _, cp = prebuilt.nuts(d, 0.5, step_size=0.25, leaf_steps=steps, max_depth=6, iterations=1,
+                                 entry="leapfrog")
+        tag = f"d{d}_L{steps}"
+        got, _, m = L.run(cp, [g[f"{tag}_q"], g[f"{tag}_p"], g[f"{tag}_e"]], depth=4, engine="warp",
+                          codegen=codegen, return_machine=True)
+        assert any(int(o["opcode"]) == 64 for o in m._dp.ops)  # the fused superblock ran
+        want = g[f"{tag}_out"]
+        scale = np.abs(want).max(axis=1, keepdims=True)
+        err = (np.abs(got - want) / scale).max()
+        assert err <= 1e-12 * steps, (tag, err)
+
+
+@pytest.mark.parametrize("engine", ["exact", "warp"])
+def test_device_dot_bit_exact_on_reference_rows(engine):
+    """`dot` = numpy's pairwise `(a*b).sum(axis=1)` (reference runtime.py:248-250), bit for
+    bit on every row of the reference fixture (n = 1 .. 2500)."""
+    g = load_npz("dot_rows.npz")
+    cp = L.compile_program(L.compile_source("def f(a, b) { return dot(a, b); }", "f"))
+    off = 0
+    by_n: dict[int, list] = {}
+    for k, n in enumerate(g["lens"].tolist()):
+        by_n.setdefault(n, []).append((g["a"][off:off + n], g["b"][off:off + n], g["res"][k]))
+        off += n
+    for n, rows in by_n.items():
+        a = np.stack([r[0] for r in rows])
+        b = np.stack([r[1] for r in rows])
+        got, _ = L.run(cp, [a, b], depth=4, engine=engine)
+        assert got.tobytes() == np.array([r[2] for r in rows]).tobytes(), n
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_warp_engine_nuts_refill(codegen):
+    """Chains outnumber the resident lanes 3:1 (4 groups of 32, persistent refill from the
+    chain queue): sampled chains from every refill wave equal the oracle's lane for lane."""
+    from paper_1910_11141_b200 import prebuilt
+
+    kw = dict(prebuilt.TEST_NUTS[1])  # d=100, T=3
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+    z = 3 * 4 * 32
+    ins = [np.zeros((z, t.dim)), np.arange(z, dtype=np.int64) * 104729 + 17]
+    got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=codegen, groups=1,
+                       exact_logpdf=False, lane_trace_cap=1 << 14, return_machine=True)
+    assert m._h.groups == 4  # 128 resident lanes for 384 chains
+    pick = np.r_[0:32, 160:192, 352:384]
+    ref = oracle_run(cp, [ins[0][pick], ins[1][pick]], cfg.min_stack_depth, lane_traces=True)
+    traces = m.lane_traces()
+    for i, lane in enumerate(pick):
+        assert np.array_equal(traces[lane], ref.lane_blocks[i]), lane
+    assert (np.abs(got[pick] - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
+
+
+@pytest.mark.parametrize("name", ["util_z30", "util_z1", "util_d5_z64"])
+def test_local_schedule_on_device_reproduces_alg1(golden_meta, name):
+    """schedule="local": the device runs paper Alg. 1 (reference local_exec.run_local) on the
+    flat program; its gradient utilisation equals the reference local engine's exactly, and
+    the pc schedule's equals the reference pc_vm's — the Fig. 6 gate (test_acceptance.py:236-266)."""
+    m = golden_meta["local"][name]
+    a = load_npz("local_runs.npz")
+    t = L.correlated_gaussian(m["dim"], m["rho"])
+    cfg = L.NutsConfig(**m["config"])
+    cp = L.compile_program(L.compile_source(L.nuts_lite_source(cfg, t), "nuts_main"))
+    ins = [np.zeros((m["z"], m["dim"])), a[f"{name}_key"]]
+    want = a[f"{name}_pc_out"]
+    out_l, tr_l = L.run(cp, ins, depth=cfg.min_stack_depth, schedule="local")
+    out_p, tr_p = L.run(cp, ins, depth=cfg.min_stack_depth, schedule="min_pc")
+    for out in (out_l, out_p):
+        assert (np.abs(out - want) / np.maximum(np.abs(want), 1.0)).max() < CHAIN_RTOL
+    u_local = L.utilization(tr_l, {t.grad})
+    u_pc = L.utilization(tr_p, {t.grad})
+    assert u_local == pytest.approx(m["util_local"], rel=1e-12)
+    assert u_pc == pytest.approx(m["util_pc"], rel=1e-12)
+    if m["z"] == 30:
+        assert u_pc / u_local >= 1.5
+    if m["z"] == 1:
+        assert u_pc == u_local == 1.0
