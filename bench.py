@@ -65,7 +65,8 @@ def parse():
                     help="warp engine with the op interpreter instead of specialised block code")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-chains", type=int, default=1024)
+    ap.add_argument("--cpu-chains", type=int, default=256)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the 2^10..2^20 chain sweep")
     ap.add_argument("--cpu-iterations", type=int, default=10)
     return ap.parse_args()
 
@@ -190,8 +191,11 @@ def measured_peaks() -> dict:
         return {}
 
 
-def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int):
-    """Time the oracle port of the reference pc engine (numpy masked mode) on host cores."""
+def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int, engine: str = "pc",
+                         want_output: bool = False):
+    """Time the oracle port of the reference engines on host cores: `pc` = pc_vm.run (numpy
+    masked mode, reference pc_vm.py:368-383), `local` = run_local (Alg. 1, local_exec.py:142-185).
+    Chains 0..chains-1 of the benchmark workload (same keys). Returns (useful grads, seconds[, out])."""
     import paper_1910_11141_b200 as L
     from oracle import lockstep_oracle as O
     from paper_1910_11141_b200.pc_vm import infer_types
@@ -199,9 +203,17 @@ def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int):
 
     small = L.NutsConfig(step_size=cfg.step_size, leaf_steps=cfg.leaf_steps, max_depth=cfg.max_depth,
                          iterations=iterations, seed=0)
-    scp = L.compile_program(L.compile_source(L.nuts_lite_source(small, target), "nuts_main"))
+    src = L.nuts_lite_source(small, target)
     q0 = np.zeros((chains, target.dim))
     key = chain_keys(0, chains)
+    if engine == "local":
+        cg = L.compile_source(src, "nuts_main")
+        t0 = time.perf_counter()
+        out, steps = O.run_local(cg, [q0, key], targets={target.name: target}, max_steps=None)
+        dt = time.perf_counter() - t0
+        grads = sum(a * g for _, a, g in steps)
+        return (grads, dt, out) if want_output else (grads, dt)
+    scp = L.compile_program(L.compile_source(src, "nuts_main"))
     types = infer_types(scp.flat, [vtype_of(q0), vtype_of(key)])
     t0 = time.perf_counter()
     res = O.run(scp, [q0, key], depth=small.min_stack_depth, types=types,
@@ -212,16 +224,59 @@ def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int):
         blk = scp.flat.blocks[b]
         grads += active * sum(1 for op in blk.ops if getattr(op, "prim", None) is not None
                               and op.prim.name == target.grad)
-    return grads, dt
+    return (grads, dt, res.output) if want_output else (grads, dt)
+
+
+def host_info() -> dict:
+    """CPU model, usable cores and the numpy / BLAS build the CPU baseline ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        cfg = np.show_config(mode="dicts")["Build Dependencies"]["blas"]
+        blas = f"{cfg.get('name')} {cfg.get('version')}"
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)), "numpy": np.__version__,
+            "blas": blas, "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
+
+
+def cpu_baseline(args, cfg, target, cp, reps: int = 3) -> tuple[dict, np.ndarray]:
+    """Warm best-of-`reps` of the pc engine port plus one run_local, both on the same
+    bounded sample (chains 0..cpu_chains-1 of the workload, cpu_iterations iterations)."""
+    cpu_reference_sample(args, cfg, target, cp, 16, 2)  # warm: imports, numpy dispatch
+    best, out = None, None
+    for _ in range(reps):
+        g, dt, o = cpu_reference_sample(args, cfg, target, cp, args.cpu_chains, args.cpu_iterations,
+                                        want_output=True)
+        if best is None or dt < best[1]:
+            best, out = (g, dt), o
+    gl, dtl = cpu_reference_sample(args, cfg, target, cp, args.cpu_chains, args.cpu_iterations, "local")
+    info = host_info()
+    return {"value": best[0] / best[1], "unit": UNIT, "cores": info["cores"], "kind": "port",
+            "sample": (f"oracle port of reference pc_vm.run (numpy masked mode), {target.name}, chains "
+                       f"0..{args.cpu_chains - 1} of this workload x {args.cpu_iterations} iterations: "
+                       f"best of {reps} warm runs {best[1]:.2f} s"),
+            "local_engine": {"value": gl / dtl, "unit": UNIT, "seconds": dtl,
+                             "sample": "oracle port of reference local_exec.run_local (Alg. 1), same chains"},
+            "host": info}, out
 
 
 def run_reference_arm(args):
+    """The reference's own algorithm on host cores (oracle port of pc_vm.run; the reference is
+    pure Python/numpy and cannot travel to the GPU box), bounded sample per step."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, target, cp = program(args)
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    cfg, target, cp = program(args)
     for _ in range(args.warmup):
         cpu_reference_sample(args, cfg, target, cp, min(args.cpu_chains, 64), args.cpu_iterations)
     tot_g, tot_t = 0, 0.0
@@ -232,13 +287,20 @@ def run_reference_arm(args):
     value = tot_g / tot_t
     sample = (f"oracle port of reference pc_vm.run (numpy masked mode), {target.name}, "
               f"{args.cpu_chains} chains x {args.cpu_iterations} iterations per step")
+    config = {"workload": f"NUTS-lite on {args.dim}-d correlated gaussian (rho=0.5, {target.name})",
+              "chains_per_step": args.cpu_chains, "iterations": args.cpu_iterations,
+              "max_tree_depth": args.depth, "step_size": 0.25, "leaf_steps": 4, "precision": "fp64",
+              "engine": "oracle port of reference pc_vm.run (numpy masked mode, min-pc schedule)",
+              "note": ("the same program and keys as the b200 arm's chains 0..chains_per_step-1; the "
+                       "CPU cannot run the b200 arm's chain count within a bounded step")}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (q0=0, unique per-chain keys)",
-        "config": workload_config(args, target),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": config,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -375,13 +437,43 @@ def main():
                "d2h_bytes_per_step": int(out.nbytes),
                "path": "paper_1910_11141_b200.run(compiled, [q0, key]) with host numpy arrays"}
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        g_cpu, dt_cpu = cpu_reference_sample(args, cfg, target, cp, args.cpu_chains, args.cpu_iterations)
-        cpu = {"value": g_cpu / dt_cpu, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
-               "kind": "port",
-               "sample": (f"oracle port of reference pc_vm.run (numpy), {target.name}, "
-                          f"{args.cpu_chains} chains x {args.cpu_iterations} iterations, {dt_cpu:.1f}s")}
+        cpu, cpu_out = cpu_baseline(args, cfg, target, cp)
+        if args.cpu_iterations == args.iterations:
+            # the CPU sample is chains 0..n-1 of this very workload: check the device's rows
+            n = cpu_out.shape[0]
+            dev_rows = torch.empty((n, cpu_out.shape[1]), dtype=torch.float64, device=dev)
+            mach.copy_output_rows_to(dev_rows.data_ptr(), n)
+            got = dev_rows.cpu().numpy()
+            err = float((np.abs(got - cpu_out) / np.maximum(np.abs(cpu_out), 1.0)).max())
+            parity = {"chains": int(n), "max_rel_err": err, "tolerance": 1e-9, "ok": bool(err < 1e-9),
+                      "against": "the CPU baseline's oracle run of the same chains (reference pc_vm.run port)"}
+
+    # BASELINE config 2: grad evals/s vs chains (2^10 .. 2^20), one warm + one timed launch each
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        keys_all = chain_keys(0, 1 << 20)
+        flops_per_grad = target.grad_flops
+        sweep = {"precision": "fp64", "schedule": args.schedule, "points": []}
+        for lg in range(10, 21):
+            zz = 1 << lg
+            mz = _native.MachineHandle(prog, zz, cfg.min_stack_depth, sched=args.schedule, ctas=args.groups,
+                                       exact_logpdf=args.exact_logpdf, warp_groups=warp)
+            mz.set_block_keys(block_keys(cp.flat, cp.labels, args.schedule,
+                                         np.flatnonzero(np.asarray(dp.blocks["grads"]) > 0)))
+            qz = torch.zeros((zz, args.dim), dtype=torch.float64, device=dev)
+            kz = torch.from_numpy(keys_all[:zz]).to(dev)
+            mz.set_input_device(0, qz.data_ptr(), qz.numel() * 8)
+            mz.set_input_device(1, kz.data_ptr(), kz.numel() * 8)
+            mz.run(-1)
+            mz.reset()
+            flush_l2(torch, dev)
+            stz = mz.run(-1)
+            v = stz.useful_grads / (stz.kernel_ms / 1e3)
+            sweep["points"].append({"chains": zz, "value": v, "ms": stz.kernel_ms,
+                                    "frac": v * flops_per_grad / 1e12 / FP64_PEAK_FALLBACK})
+            del mz, qz, kz
 
     # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)
     from paper_1910_11141_b200.distributed import diagnostics
@@ -404,7 +496,7 @@ def main():
             "data": "synthetic (q0=0, unique per-chain keys, random-free target parameters)",
             "config": {**workload_config(args, target), "parallelism": f"chains sharded over {world} GPU(s)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "diagnostics": diag_summary,
+            "clocks": clk, "diagnostics": diag_summary, "parity": parity, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

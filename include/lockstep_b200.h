@@ -230,7 +230,8 @@ int ls_read_output(ls_machine* m, void* host, int64_t bytes);
 int ls_machine_set_output_host(ls_machine* m, void* host, int64_t bytes);
 /* device pointer of the z x width output (valid until destroy) */
 int ls_output_device(ls_machine* m, void** dev);
-/* device-to-device copy of the output (e.g. into a torch CUDA tensor for NCCL diagnostics) */
+/* device-to-device copy of the output's first bytes / (width * 8) rows (e.g. into a torch
+   CUDA tensor for NCCL diagnostics) */
 int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes);
 /* drain recorded (block, active) step pairs; *n = number written */
 int ls_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* active, int64_t cap, int64_t* n);

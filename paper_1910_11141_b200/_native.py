@@ -317,6 +317,11 @@ class MachineHandle:
         self._c(self.lib.ls_read_output(self.handle, _ptr(out), out.nbytes))
         return out.view(dtype)
 
+    def copy_output_rows_to(self, dev_ptr: int, rows: int) -> None:
+        """The first `rows` output rows into device memory at dev_ptr."""
+        width = int(self.program.dp.vars[self.program.dp.output]["width"])
+        self._c(self.lib.ls_copy_output_device(self.handle, C.c_void_p(dev_ptr), rows * width * 8))
+
     def copy_output_to(self, dev_ptr: int, nbytes: int) -> None:
         self._c(self.lib.ls_copy_output_device(self.handle, C.c_void_p(dev_ptr), nbytes))
 

@@ -50,6 +50,8 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        "ewu": int(os.environ.get("LSB_CG_EWU", "16")),
        # dev-only superblock phase clocks (tools/sb_profile.py)
        "sbprof": int(os.environ.get("LSB_CG_SBPROF", "0")),
+       # dev-only per-block SM-cycle accounting (clock64 + atomics; tools/block_profile.py)
+       "bprof": int(os.environ.get("LSB_CG_BPROF", "0")),
        # n-tiles per superblock kick pass
        "lfkc": int(os.environ.get("LSB_CG_LFKC", "2")),
        # shared out-of-line vector helpers instead of a loop per call site
@@ -787,7 +789,7 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
            f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}",
-           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_LF_KC={OPT['lfkc']}",
+           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_BLOCK_PROFILE={OPT['bprof']}", f"-DLSB_LF_KC={OPT['lfkc']}",
            f"-DLSB_SB_INLINE={OPT['sbinline']}", f"-DLSB_WG_INLINE={OPT['wginline']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))

@@ -1096,7 +1096,8 @@ int ls_host_free(void* host) {
 int ls_copy_output_device(ls_machine* m, void* dev_dst, int64_t bytes) {
   if (!m || !dev_dst) return fail(LS_EINVAL, "null machine");
   CK(cudaSetDevice(m->device));
-  if (bytes != m->z * m->out_width * 8) return fail(LS_EINVAL, "output size mismatch");
+  if (bytes <= 0 || bytes > m->z * m->out_width * 8 || bytes % (m->out_width * 8))
+    return fail(LS_EINVAL, "output size mismatch (whole rows, at most z of them)");
   CK(cudaMemcpyAsync(dev_dst, m->out_host_dev ? m->out_host_dev : m->output, bytes, cudaMemcpyDefault,
                      m->stream));
   CK(cudaStreamSynchronize(m->stream));

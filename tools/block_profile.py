@@ -2,25 +2,27 @@
 
 Runs one warm launch and prints, per flat block, steps, mean active lanes, total
 SM cycles (sum over warps) and share, from the device's clock64 accounting.
-usage: python tools/block_profile.py [chains] [codegen 0/1]
+usage: python tools/block_profile.py [chains] [codegen 0/1] [schedule]  (builds a LSB_CG_BPROF=1 library)
 """
 import os
 import sys
 
 import numpy as np
 
+os.environ.setdefault("LSB_CG_BPROF", "1")  # a profiling build of the library (clock64 per block)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1910_11141_b200 as L  # noqa: E402
 from paper_1910_11141_b200 import prebuilt  # noqa: E402
 
 z = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 cg = (sys.argv[2] != "0") if len(sys.argv) > 2 else True
+sched = sys.argv[3] if len(sys.argv) > 3 else "priority"
 kw = dict(prebuilt.BENCH)
 cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
 q0 = np.zeros((z, t.dim))
 key = np.arange(z, dtype=np.int64) * 7919 + 11
 m = L.init_machine(cp, [q0, key], depth=cfg.min_stack_depth, engine="warp", optimize=True,
-                   exact_logpdf=False, codegen=cg)
+                   exact_logpdf=False, codegen=cg, schedule=sched)
 m._h.run(-1)
 m._h.reset()
 st = m._h.run(-1)
