@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 METRIC = "NUTS gradient evals/sec vs #chains at 1/2/4/8 B200 (+ % of roofline)"
 UNIT = "grad_evals/s"
 FP64_PEAK_FALLBACK = 37.0  # TFLOP/s, tools/fp64_peaks.cu on this pool's B200 (DFMA 36.9, DMMA 37.0)
+FP32_PEAK_FALLBACK = 2250.0 / 2 / 3  # 3xTF32: nominal dense bf16 / 2 (TF32) / 3 MMAs per product
 
 
 def parse():
@@ -67,6 +68,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-chains", type=int, default=256)
     ap.add_argument("--no-sweep", action="store_true", help="skip the 2^10..2^20 chain sweep")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 (tcgen05) arm")
     ap.add_argument("--cpu-iterations", type=int, default=10)
     return ap.parse_args()
 
@@ -209,7 +211,7 @@ def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int, en
     if engine == "local":
         cg = L.compile_source(src, "nuts_main")
         t0 = time.perf_counter()
-        out, steps = O.run_local(cg, [q0, key], targets={target.name: target}, max_steps=None)
+        out, steps = O.run_local(cg, [q0, key], targets={target.name: L.device_target(target.name)}, max_steps=None)
         dt = time.perf_counter() - t0
         grads = sum(a * g for _, a, g in steps)
         return (grads, dt, out) if want_output else (grads, dt)
@@ -217,7 +219,7 @@ def cpu_reference_sample(args, cfg, target, cp, chains: int, iterations: int, en
     types = infer_types(scp.flat, [vtype_of(q0), vtype_of(key)])
     t0 = time.perf_counter()
     res = O.run(scp, [q0, key], depth=small.min_stack_depth, types=types,
-                targets={target.name: target}, max_steps=None)
+                targets={target.name: L.device_target(target.name)}, max_steps=None)
     dt = time.perf_counter() - t0
     grads = 0
     for b, active in res.steps:
@@ -401,7 +403,7 @@ def main():
     ms_per_step = 1e3 * t_total / args.steps
 
     # roofline of the dominant kernel (vm_kernel: the whole step is one launch)
-    flops_per_grad = target.grad_flops
+    flops_per_grad = L.device_target(target.name).grad_flops
     achieved = (grads / args.steps) * flops_per_grad / (np.mean(times) / 1e3) / 1e12
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_FALLBACK, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_FALLBACK, "traffic": None,
@@ -450,30 +452,51 @@ def main():
             parity = {"chains": int(n), "max_rel_err": err, "tolerance": 1e-9, "ok": bool(err < 1e-9),
                       "against": "the CPU baseline's oracle run of the same chains (reference pc_vm.run port)"}
 
-    # BASELINE config 2: grad evals/s vs chains (2^10 .. 2^20), one warm + one timed launch each
-    sweep = None
-    if rank == 0 and world == 1 and not args.no_sweep:
-        keys_all = chain_keys(0, 1 << 20)
-        flops_per_grad = target.grad_flops
-        sweep = {"precision": "fp64", "schedule": args.schedule, "points": []}
-        for lg in range(10, 21):
-            zz = 1 << lg
-            mz = _native.MachineHandle(prog, zz, cfg.min_stack_depth, sched=args.schedule, ctas=args.groups,
-                                       exact_logpdf=args.exact_logpdf, warp_groups=warp)
-            mz.set_block_keys(block_keys(cp.flat, cp.labels, args.schedule,
-                                         np.flatnonzero(np.asarray(dp.blocks["grads"]) > 0)))
-            qz = torch.zeros((zz, args.dim), dtype=torch.float64, device=dev)
-            kz = torch.from_numpy(keys_all[:zz]).to(dev)
-            mz.set_input_device(0, qz.data_ptr(), qz.numel() * 8)
-            mz.set_input_device(1, kz.data_ptr(), kz.numel() * 8)
-            mz.run(-1)
+    # BASELINE config 2: grad evals/s vs chains (2^10 .. 2^20) in fp64 and fp32, one warm + one
+    # timed launch per point; plus the fp32 arm at this run's chain count
+    sweep, fp32 = None, None
+    keys_dp = np.flatnonzero(np.asarray(dp.blocks["grads"]) > 0)
+
+    def one_point(zz, precision, reps=1):
+        mz = _native.MachineHandle(prog, zz, cfg.min_stack_depth, sched=args.schedule, ctas=args.groups,
+                                   exact_logpdf=args.exact_logpdf, warp_groups=warp, precision=precision)
+        mz.set_block_keys(block_keys(cp.flat, cp.labels, args.schedule, keys_dp))
+        qz = torch.zeros((zz, args.dim), dtype=torch.float64, device=dev)
+        kz = torch.from_numpy(chain_keys(first, zz)).to(dev)
+        mz.set_input_device(0, qz.data_ptr(), qz.numel() * 8)
+        mz.set_input_device(1, kz.data_ptr(), kz.numel() * 8)
+        mz.run(-1)
+        ms, gsum = 0.0, 0
+        for _ in range(reps):
             mz.reset()
             flush_l2(torch, dev)
             stz = mz.run(-1)
-            v = stz.useful_grads / (stz.kernel_ms / 1e3)
-            sweep["points"].append({"chains": zz, "value": v, "ms": stz.kernel_ms,
-                                    "frac": v * flops_per_grad / 1e12 / FP64_PEAK_FALLBACK})
-            del mz, qz, kz
+            ms += stz.kernel_ms
+            gsum += stz.useful_grads
+        del mz, qz, kz
+        return gsum / (ms / 1e3), ms / reps
+
+    flops_per_grad = L.device_target(target.name).grad_flops
+    peaks = measured_peaks()
+    # 3xTF32 = three TF32 MMAs per product; TF32 dense runs at half the bf16 rate
+    tf32x3_peak = peaks["bf16_tflops"] / 2 / 3 if peaks.get("bf16_tflops") else FP32_PEAK_FALLBACK
+    if warp and not args.no_fp32 and world == 1:
+        v32, ms32 = one_point(z, "fp32", reps=max(1, min(args.steps, 3)))
+        fp32 = {"value": v32, "unit": UNIT, "ms_per_step": ms32, "chains": z,
+                "roofline": {"bound": "tensor", "achieved": v32 * flops_per_grad / 1e12, "peak": tf32x3_peak,
+                             "unit": "TFLOP/s", "frac": v32 * flops_per_grad / 1e12 / tf32x3_peak,
+                             "note": ("useful fp32 gradient FLOPs; peak = 3xTF32 rate = MEASURED_PEAKS "
+                                      "bf16_tflops / 2 (TF32) / 3 (split)")},
+                "arith": "fused leapfrog in float32 on tcgen05 (kind::tf32, 3xTF32), VM control in f64"}
+    if rank == 0 and world == 1 and not args.no_sweep:
+        sweep = {"schedule": args.schedule, "fp64": [], "fp32": []}
+        for lg in range(10, 21):
+            zz = 1 << lg
+            for precision in (("fp64", "fp32") if warp and not args.no_fp32 else ("fp64",)):
+                v, ms = one_point(zz, precision)
+                peak = FP64_PEAK_FALLBACK if precision == "fp64" else tf32x3_peak
+                sweep[precision].append({"chains": zz, "value": v, "ms": ms,
+                                         "frac": v * flops_per_grad / 1e12 / peak})
 
     # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)
     from paper_1910_11141_b200.distributed import diagnostics
@@ -496,7 +519,7 @@ def main():
             "data": "synthetic (q0=0, unique per-chain keys, random-free target parameters)",
             "config": {**workload_config(args, target), "parallelism": f"chains sharded over {world} GPU(s)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "diagnostics": diag_summary, "parity": parity, "sweep": sweep,
+            "clocks": clk, "diagnostics": diag_summary, "parity": parity, "fp32": fp32, "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -18,10 +18,10 @@ It re-states, in masked mode, the reference engine of arXiv 1910.11141's
 * target kernels (`workloads.py:186-228`): gaussian `norm - 0.5*einsum`,
   `-(x @ P)`; logistic `logaddexp` / stable sigmoid with two GEMMs.
 
-It consumes the flat program produced by this repo's host compiler (which is
-itself checked to be text-identical to the reference's, see
-tests/test_host_pipeline.py), so it runs on the GPU box where
-`/root/reference` does not exist.
+It consumes the flat program of the reference's own compiler (the package
+imports the installed `lockstep`, paper_1910_11141_b200/reference.py) and
+re-states the engine and kernels independently of the reference's engine
+code, so it can check the device on the GPU box.
 
 Parity is pinned: `tests/test_oracle.py` checks this oracle bit-for-bit
 against fixtures minted from the real reference (`tests/golden/make_golden.py`):

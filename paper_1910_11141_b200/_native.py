@@ -24,7 +24,8 @@ HEADER = Path(__file__).resolve().parent.parent / "include" / "lockstep_b200.h"
 LS_OK, LS_EINVAL, LS_ECUDA, LS_ENOMEM = 0, -1, -2, -3
 RUN_HALTED, RUN_PAUSED, RUN_OVERFLOW, RUN_UNDERFLOW, RUN_STEP_LIMIT = 0, 1, 2, 3, 4
 SCHED = {"min_pc": 0, "most_populated": 1, "local": 2, "priority": 3}
-MF_NO_STAGE = 1  # ls_machine_opts.flags (lockstep_b200.h)
+MF_NO_STAGE, MF_FP32 = 1, 2  # ls_machine_opts.flags (lockstep_b200.h)
+PRECISIONS = ("fp64", "fp32")
 
 
 class ProgramDesc(C.Structure):
@@ -238,7 +239,7 @@ class MachineHandle:
     def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
                  lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
                  exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False,
-                 stage_targets: bool = True):
+                 stage_targets: bool = True, precision: str = "fp64"):
         if sched not in SCHED:
             raise ValueError(f"unknown schedule '{sched}'")
         self.program = program
@@ -246,7 +247,13 @@ class MachineHandle:
         self.z = z
         self.depth = depth
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
-                           int(lane_trace_cap), int(warp_groups), 0 if stage_targets else MF_NO_STAGE)
+                           int(lane_trace_cap), int(warp_groups),
+                           (0 if stage_targets else MF_NO_STAGE) | (MF_FP32 if precision == "fp32" else 0))
+        if precision not in PRECISIONS:
+            raise ValueError(f"unknown precision '{precision}' (one of {PRECISIONS})")
+        if precision == "fp32" and not warp_groups:
+            raise ValueError("the fp32 arm runs on the warp engine (engine='warp')")
+        self.precision = precision
         self.lane_trace_cap = int(lane_trace_cap)
         self.warp_groups = bool(warp_groups)
         self._host_out: np.ndarray | None = None

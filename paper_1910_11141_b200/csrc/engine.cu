@@ -205,22 +205,18 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
 
 // up to 16 warps per CTA (one CTA per SM when a target is staged); 128 registers
 constexpr int kWarpCtaMax = 16;
-__global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __grid_constant__ VMArgs a) {
-  extern __shared__ double lf_smem[];
-  // stage the target's B fragments once per CTA; every warp's DMMA reads them at LDS latency
-  if (a.stage_doubles > 0) {
-    const double2* src = reinterpret_cast<const double2*>(a.stage_src);
-    double2* dst = reinterpret_cast<double2*>(lf_smem);
-    for (int i = threadIdx.x; i < a.stage_doubles / 2; i += blockDim.x) dst[i] = __ldg(src + i);
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (g >= a.n_groups) return;
+
+// One warp's 32-lane group: the step loop of the warp engine. With a.wg the 4 warps of a
+// warpgroup choose one block per step together (a named barrier per step) — the fp32 arm's
+// tensor-core superblock runs the warpgroup's 128 chains at once.
+__device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wq = wid & 3, wgi = wid >> 2;
+  const int g = blockIdx.x * (blockDim.x >> 5) + wid;
   constexpr int L = 32;
   const Lane ln{a.ws + (size_t)g * a.group_rows * L, a.sp + (size_t)g * a.n_sp_rows * L,
                 a.pcs + (size_t)g * (a.depth + 1) * L, lane, L};
-  double* my_smem = lf_smem + a.stage_doubles + (size_t)(threadIdx.x >> 5) * a.lf_smem_per_warp;
+  double* my_smem = lf_smem + a.stage_doubles + (size_t)wid * a.lf_smem_per_warp;
   int* pc_sp = &ln.sp_row(a.n_sp_rows - 1);
   long long* my_chain = a.chain_of + (size_t)g * L + lane;
   long long steps = a.group_steps[g];
@@ -230,7 +226,6 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
   long long* bcycles = a.blk_cycles + (size_t)g * a.n_blocks;
 #endif
   unsigned long long useful = 0, launched = 0;
-  if (a.group_done[g]) return;
   // the lane's chain id lives in a register; chain_of is updated whenever it changes
   long long chain = *my_chain;
 #ifdef LSB_GENERATED
@@ -242,9 +237,11 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
     pc_r = ln.pcs[(psp_r - 1) * L + lane];
   }
 #endif
+  int par = 0;           // warpgroup step-slot parity
+  bool faulted = false;  // warpgroup mode: stop the warpgroup at the next step
 
   for (;;) {
-    if (chain == -1) {
+    if (chain == -1 && !faulted) {
       const unsigned long long c = atomicAdd(a.next_chain, 1ull);
       if ((long long)c < a.z) {
         chain = (long long)c;
@@ -260,43 +257,60 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
     }
 #ifdef LSB_GENERATED
     const int pc = chain >= 0 ? pc_r : a.halt;
+    const int depth_now = psp_r;
 #else
     const int pc = chain >= 0 ? ln.pcs[(*pc_sp - 1) * L + lane] : a.halt;
+    const int depth_now = chain >= 0 ? *pc_sp : 0;
 #endif
     int b;
+    unsigned key = 0, best = 0;
     if (a.sched == LS_SCHED_MOST_POPULATED) {
       const unsigned peers = __match_any_sync(kFull, pc);
-      const unsigned key = pc == a.halt ? 0u : ((unsigned)__popc(peers) << 16) | (0xffffu - (unsigned)pc);
-      const unsigned best = __reduce_max_sync(kFull, key);
-      b = best == 0 ? a.halt : (int)(0xffffu - (best & 0xffffu));
+      const unsigned k2 = pc == a.halt ? 0u : ((unsigned)__popc(peers) << 16) | (0xffffu - (unsigned)pc);
+      const unsigned bm = __reduce_max_sync(kFull, k2);
+      b = bm == 0 ? a.halt : (int)(0xffffu - (bm & 0xffffu));
     } else {
       // keyed rules (min_pc, priority, local): the populated block with the least key;
-      // keys carry the block index in their low 16 bits (host: pc_vm.block_keys)
-#ifdef LSB_GENERATED
-      const int depth_now = psp_r;
-#else
-      const int depth_now = chain >= 0 ? *pc_sp : 0;
-#endif
-      const unsigned key = pc == a.halt ? 0xffffffffu : lane_key(a, pc, depth_now);
-      const unsigned best = __reduce_min_sync(kFull, key);
+      // keys carry the block index in their low 16 bits (host: schedule.block_keys)
+      key = pc == a.halt ? 0xffffffffu : lane_key(a, pc, depth_now);
+      best = __reduce_min_sync(kFull, key);
+      if (a.wg) {  // the warpgroup agrees on one block (and on stopping)
+        const bool stop = faulted || ((steps & 15) == 0 && *(volatile int*)a.abort_flag) ||
+                          (a.max_steps >= 0 && steps >= a.max_steps);
+        if (lane == 0) {
+          lsb_tcs.key[wgi][par][wq] = best;
+          lsb_tcs.stop[wgi][par][wq] = stop;
+        }
+        wg_bar(wgi);
+        unsigned m = 0xffffffffu;
+        int any_stop = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          m = min(m, lsb_tcs.key[wgi][par][w]);
+          any_stop |= lsb_tcs.stop[wgi][par][w];
+        }
+        par ^= 1;
+        if (any_stop && m != 0xffffffffu) {
+          if (!faulted && a.max_steps >= 0 && steps >= a.max_steps && lane == 0) a.paused[0] = 1;
+          break;
+        }
+        best = m;
+      }
       b = best == 0xffffffffu ? a.halt : (int)(best & 0xffffu);
     }
     if (b == a.halt) {
       if (lane == 0) a.group_done[g] = 1;
       break;
     }
-    // another group's fault stops this one within 16 steps (one flag read per 16 steps)
-    if ((steps & 15) == 0 && *(volatile int*)a.abort_flag) break;
-    if (a.max_steps >= 0 && steps >= a.max_steps) {
-      if (lane == 0) a.paused[0] = 1;
-      break;
+    if (!a.wg) {
+      // another group's fault stops this one within 16 steps (one flag read per 16 steps)
+      if ((steps & 15) == 0 && *(volatile int*)a.abort_flag) break;
+      if (a.max_steps >= 0 && steps >= a.max_steps) {
+        if (lane == 0) a.paused[0] = 1;
+        break;
+      }
     }
-#ifdef LSB_GENERATED
-    const bool active = pc == b && (a.sched != LS_SCHED_LOCAL || psp_r == __shfl_sync(kFull, psp_r, __ffs(__ballot_sync(kFull, pc == b)) - 1));
-#else
-    const bool active = pc == b && (a.sched != LS_SCHED_LOCAL ||
-                                    *pc_sp == __shfl_sync(kFull, *pc_sp, __ffs(__ballot_sync(kFull, pc == b)) - 1));
-#endif
+    const bool active = a.sched == LS_SCHED_MOST_POPULATED ? pc == b : (pc != a.halt && key == best);
     const int count = __popc(__ballot_sync(kFull, active));
     if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, b);
     StepFault f;
@@ -329,7 +343,9 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
         atomicExch(a.abort_flag, 1);
       }
       ++steps;
-      break;
+      if (!a.wg) break;
+      faulted = true;  // tell the warpgroup at the next step
+      continue;
     }
     const unsigned hmask = __ballot_sync(kFull, halted_now);
     if (hmask) {
@@ -359,6 +375,22 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
     if (useful) atomicAdd(a.useful, useful);
     if (launched) atomicAdd(a.launched, launched);
   }
+}
+
+__global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __grid_constant__ VMArgs a) {
+  extern __shared__ double lf_smem[];
+  // stage the target's B fragments once per CTA; every warp's DMMA reads them at LDS latency
+  if (a.stage_doubles > 0) {
+    const double2* src = reinterpret_cast<const double2*>(a.stage_src);
+    double2* dst = reinterpret_cast<double2*>(lf_smem);
+    for (int i = threadIdx.x; i < a.stage_doubles / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
+  if (a.tc_img != nullptr) tc_cta_begin(a, reinterpret_cast<unsigned char*>(lf_smem));
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // warpgroup mode: every warp of a warpgroup takes part in its steps (groups come in 4s)
+  if (g < a.n_groups && (a.wg || !a.group_done[g])) warp_group_run(a, lf_smem);
+  if (a.tc_img != nullptr) tc_cta_end();
 }
 
 __global__ void init_static_kernel(const __grid_constant__ VMArgs a) {
@@ -435,6 +467,7 @@ struct ls_program {
   int n_stacked = 0;
   int flat_rows = 0;
   DevTarget targets[kMaxTargets];
+  std::vector<double> host_params[kMaxTargets];  // row-major P (gaussian) for the fp32 image
   std::vector<double*> owned;
 };
 
@@ -480,8 +513,13 @@ struct ls_machine {
   bool refill = false;
   int lf_smem_per_warp = 0;
   int warps_per_cta = 4;     // warp engine CTA shape
+  size_t smem_bytes = 0;     // warp engine dynamic shared memory per CTA
   int stage_target = -1;     // target whose B fragments each CTA stages in shared memory
   int stage_doubles = 0;
+  // fp32 arm (LS_MF_FP32): tensor-core superblocks, warpgroup stepping
+  bool fp32 = false;
+  void* tc_img = nullptr;
+  int tc_img_bytes = 0, tc_half_bytes = 0, tc_lbo = 0, tc_sbo = 0, tc_smem_off = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   long long launches = 0;
@@ -570,6 +608,10 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   a.lane_trace = m->lane_trace; a.lane_trace_len = m->lane_trace_len; a.lane_trace_cap = m->lane_trace_cap;
   a.fault = m->fault; a.abort_flag = m->flags + 0; a.paused = m->flags + 1;
   a.bkey = m->bkey;
+  a.wg = m->fp32 ? 1 : 0;
+  a.tc_img = m->tc_img;
+  a.tc_img_bytes = m->tc_img_bytes; a.tc_half_bytes = m->tc_half_bytes;
+  a.tc_lbo = m->tc_lbo; a.tc_sbo = m->tc_sbo; a.tc_smem_off = m->tc_smem_off;
   return a;
 }
 
@@ -674,6 +716,7 @@ int ls_program_bind_target(ls_program* p, int32_t slot, int32_t kind, int32_t di
     if ((rc = frag(n, dim, [&](int k, int c) { return h[(size_t)k * dim + c]; }, &t.B2, &t.KS2, &t.NT2))) return rc;
   }
   p->targets[slot] = t;
+  p->host_params[slot] = h;
   return LS_OK;
 }
 
@@ -696,7 +739,7 @@ int ls_machine_destroy(ls_machine* m) {
   cudaFree(m->group_steps); cudaFree(m->group_done); cudaFree(m->trace_block);
   cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
   cudaFree(m->blk_active); cudaFree(m->blk_cycles); cudaFree(m->fault); cudaFree(m->flags);
-  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len); cudaFree(m->bkey);
+  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len); cudaFree(m->bkey); cudaFree(m->tc_img);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -803,7 +846,50 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
         m->warps_per_cta = wpc;
       }
     }
-    const size_t smem = ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double);
+    if (m->opts.flags & LS_MF_FP32) {
+      // fp32 arm: the superblock target's precision matrix as a TF32 hi/lo image (UMMA K-major,
+      // no swizzle) that each CTA bulk-copies into shared memory in place of the DMMA fragments
+      if (m->opts.sched == LS_SCHED_MOST_POPULATED) {
+        delete m;
+        return fail(LS_EINVAL, "the fp32 arm steps warpgroups together: use a keyed schedule");
+      }
+      if (st < 0 || !one || p->targets[st].kind != LS_TARGET_GAUSSIAN || p->targets[st].dim > 128) {
+        delete m;
+        return fail(LS_EINVAL, "the fp32 arm needs fused leapfrogs of one gaussian target with d <= 128");
+      }
+      m->fp32 = true;
+      m->stage_target = -1;
+      m->stage_doubles = 0;
+      const int d = p->targets[st].dim, K = (d + 7) / 8 * 8, N = (d + 15) / 16 * 16;
+      std::vector<float> P32((size_t)K * N, 0.f);
+      const std::vector<double>& hp = p->host_params[st];
+      for (int k = 0; k < d; ++k)
+        for (int n = 0; n < d; ++n) P32[(size_t)k * N + n] = (float)hp[(size_t)k * d + n];
+      std::vector<uint8_t> img;
+      m->tc_lbo = 128;
+      m->tc_sbo = (K / 4) * 128;
+      m->tc_half_bytes = lsbtc::b_image_nosw(P32.data(), K, N, N, m->tc_lbo, m->tc_sbo, img);
+      m->tc_img_bytes = (int)img.size();
+      int rc2 = dalloc((uint8_t**)&m->tc_img, img.size());
+      if (rc2) {
+        delete m;
+        return rc2;
+      }
+      CK(cudaMemcpy(m->tc_img, img.data(), img.size(), cudaMemcpyHostToDevice));
+      int wpc = kWarpCtaMax;
+      auto off_of = [&](int w) { return ((size_t)w * m->lf_smem_per_warp * sizeof(double) + 1023) / 1024 * 1024; };
+      while (wpc >= 4 && off_of(wpc) + img.size() > (size_t)smem_optin) wpc -= 4;
+      if (wpc < 4) {
+        cudaFree(m->tc_img);
+        delete m;
+        return fail(LS_EINVAL, "the fp32 arm's shared-memory image does not fit");
+      }
+      m->warps_per_cta = wpc;
+      m->tc_smem_off = (int)off_of(wpc);
+    }
+    const size_t smem = m->fp32 ? (size_t)m->tc_smem_off + (size_t)m->tc_img_bytes
+                                : ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double);
+    m->smem_bytes = smem;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -815,6 +901,10 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     groups = m->opts.ctas > 0 ? 4 * m->opts.ctas
                               : (int)std::min<long long>(want, (long long)sms * m->warps_per_cta * per_sm);
     if (groups > want) groups = (int)want;
+    if (m->fp32) {  // whole CTAs of warpgroups (spare groups just find the chain queue empty)
+      const int wpc = m->warps_per_cta;
+      groups = m->opts.ctas > 0 ? wpc * m->opts.ctas : (groups + wpc - 1) / wpc * wpc;
+    }
   } else {
     int lanes = m->opts.lanes_per_cta > 0 ? m->opts.lanes_per_cta : (int)std::min<long long>(z, kMaxLanes);
     if (m->opts.lanes_per_cta <= 0 && z > kMaxLanes) {
@@ -983,8 +1073,7 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
   ls_program* p = m->p;
   VMArgs a = make_args(m, max_steps);
   m->started = true;
-  size_t smem = m->warp ? ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double)
-                        : (p->blocks.size() + 1) * sizeof(int);
+  size_t smem = m->warp ? m->smem_bytes : (p->blocks.size() + 1) * sizeof(int);
   if (smem > 48 * 1024) {
     if (m->warp) CK(cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     else CK(cudaFuncSetAttribute(vm_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

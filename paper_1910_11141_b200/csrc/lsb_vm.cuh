@@ -17,6 +17,7 @@
 
 #include "../../include/lockstep_b200.h"
 #include "lsb_dmma.cuh"
+#include "lsb_tc.cuh"
 #include "lsb_ops.cuh"
 
 #ifndef LSB_LF_KC
@@ -118,6 +119,13 @@ struct VMArgs {
   int* abort_flag;
   int* paused;
   const unsigned* bkey;         // [n_blocks] schedule key of each block (block index in bits 0..15)
+  // warpgroup stepping: the 4 warps of a warpgroup select one block per step together
+  int wg;
+  // fp32 arm (lsb_tc_leapfrog.cuh): leapfrog superblocks on tcgen05 (3xTF32), the target's
+  // precision matrix as a K-major TF32 hi/lo image staged in shared memory at byte offset
+  // tc_smem_off by one bulk copy; nullptr = fp64 (DMMA) superblocks
+  const void* tc_img;
+  int tc_img_bytes, tc_half_bytes, tc_lbo, tc_sbo, tc_smem_off;
 };
 
 // Schedule key of a live lane at block `pc` with pc-stack depth `psp` (keyed rules pick the
@@ -714,10 +722,13 @@ __host__ __device__ __forceinline__ int lf_smem_doubles(int d) {
 
 // One accumulator pass (n-tiles C0 .. C0+7) of the register-momentum superblock:
 // g = -(q P) for the tile's 8 chains, p += (e/2) g in the C-fragment layout.
+// nkick = 2 applies the same gradient twice, as two separately rounded kicks: the last
+// half-kick of leapfrog step i and the first of step i+1 contract the same q (the
+// reference recomputes it, workloads.py:464-467), so a leaf costs L+1 contractions.
 template <int NT, int C0, bool SB>
 __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
                                         const double* Bf, double half, bool last, uint64_t* gg, int d,
-                                        bool want_lp, double& quad) {
+                                        bool want_lp, double& quad, int nkick) {
   // LSB_LF_KC n-tiles per pass: p (in registers) + acc + prefetched fragments fit
   constexpr int NTC = (NT - C0) < LSB_LF_KC ? (NT - C0) : LSB_LF_KC;
   const int lane = threadIdx.x & 31, g = lane >> 2;
@@ -729,6 +740,7 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
     for (int e = 0; e < 2; ++e) {
       const double gv = -acc[j][e];
       p[C0 + j][e] = __dadd_rn(__dmul_rn(half, gv), p[C0 + j][e]);
+      if (nkick == 2) p[C0 + j][e] = __dadd_rn(__dmul_rn(half, gv), p[C0 + j][e]);
       const int col = 8 * (C0 + j) + 2 * (lane & 3) + e;
       if (last && gg != nullptr && col < d) gg[(size_t)col * 32] = f64_bits(gv);
       // the last kick contracts at the final q: accumulate q.(P q) in warp_gauss's order
@@ -741,10 +753,10 @@ __device__ __forceinline__ void lf_kick(double (&p)[NT][2], const double* Qs, in
 template <int NT, int C0, bool SB>
 __device__ __forceinline__ void lf_kicks(double (&p)[NT][2], const double* Qs, int SQ, const DevTarget& tg,
                                          const double* Bf, double half, bool last, uint64_t* gg, int d,
-                                         bool want_lp, double& quad) {
-  lf_kick<NT, C0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
+                                         bool want_lp, double& quad, int nkick) {
+  lf_kick<NT, C0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad, nkick);
   if constexpr (C0 + LSB_LF_KC < NT)
-    lf_kicks<NT, C0 + LSB_LF_KC, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
+    lf_kicks<NT, C0 + LSB_LF_KC, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad, nkick);
 }
 
 // Dev-only phase clock of the superblock (-DLSB_SB_PROFILE=1; tools/sb_profile.py):
@@ -823,27 +835,33 @@ __device__ void warp_leapfrog_rp(const VMArgs& a, const Lane& ln, const ROp& op,
 #endif
     LSB_SB_T(t_c);
     LSB_SB_ADD(1, t_b, t_c);
+    // L+1 contractions: g(q0) then, per step, drift and g(q_{i+1}), whose kick serves
+    // the end of step i and the start of step i+1 (two separately rounded kicks)
+    if (steps > 0) {
+      LSB_SB_T(t_k0);
+      lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, false, gg, d, want_lp, quad, 1);
+      __syncwarp();
+      LSB_SB_T(t_k1);
+      LSB_SB_ADD(2, t_k0, t_k1);
+    }
     for (int it = 0; it < steps; ++it) {
-      for (int hs = 0; hs < 2; ++hs) {
-        const bool last = (it == steps - 1) && hs == 1;
-        LSB_SB_T(t_k0);
-        lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad);
-        __syncwarp();
-        LSB_SB_T(t_k1);
-        LSB_SB_ADD(2, t_k0, t_k1);
-        if (hs == 0) {  // drift: q = e p + q on this thread's (row, columns)
+      LSB_SB_T(t_d0);
+      // drift: q = e p + q on this thread's (row, columns)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = 8 * nt + 2 * (lane & 3) + e;
-              if (col < d) Qs[g * SQ + col] = __dadd_rn(__dmul_rn(eg, p[nt][e]), Qs[g * SQ + col]);
-            }
-          __syncwarp();
-          LSB_SB_T(t_k2);
-          LSB_SB_ADD(3, t_k1, t_k2);
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * nt + 2 * (lane & 3) + e;
+          if (col < d) Qs[g * SQ + col] = __dadd_rn(__dmul_rn(eg, p[nt][e]), Qs[g * SQ + col]);
         }
-      }
+      __syncwarp();
+      LSB_SB_T(t_d1);
+      LSB_SB_ADD(3, t_d0, t_d1);
+      const bool last = it == steps - 1;
+      lf_kicks<NT, 0, SB>(p, Qs, SQ, tg, Bf, half, last, gg, d, want_lp, quad, last ? 1 : 2);
+      __syncwarp();
+      LSB_SB_T(t_k2);
+      LSB_SB_ADD(2, t_d1, t_k2);
     }
     if (want_lp) {  // warp_gauss's reduction over the row's 4 threads
       quad += __shfl_xor_sync(kFull, quad, 1);
@@ -906,9 +924,15 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
 #else
 #define LSB_SB_QUAL __noinline__
 #endif
+#include "lsb_tc_leapfrog.cuh"
+
 template <int NT>
 __device__ LSB_SB_QUAL void warp_leapfrog_nt(const VMArgs& a, const Lane ln, const ROp op, bool part,
                                               double* sm, long long chain) {
+  if (a.tc_img != nullptr) {  // fp32 arm: the warpgroup's 128 chains on tcgen05
+    if constexpr (NT <= 16) wg_leapfrog_tf32<NT>(a, ln, op, part, chain);
+    return;
+  }
   const double* Bs = staged_B(a, op.imm0);
   if (Bs) warp_leapfrog_rp<NT, true>(a, ln, op, part, sm, chain, Bs);
   else warp_leapfrog_rp<NT, false>(a, ln, op, part, sm, chain, a.targets[op.imm0].B1);
@@ -916,6 +940,10 @@ __device__ LSB_SB_QUAL void warp_leapfrog_nt(const VMArgs& a, const Lane ln, con
 
 __device__ inline void warp_leapfrog(const VMArgs& a, const Lane& ln, const ROp& op, bool part, double* sm,
                                      long long chain) {
+  if (a.tc_img != nullptr) {
+    wg_leapfrog_tf32_any(a, ln, op, part, chain);
+    return;
+  }
   const DevTarget& tg = a.targets[op.imm0];
   const double* Bs = staged_B(a, op.imm0);
   switch (tg.NT1) {  // d <= 128: register-momentum variant
@@ -980,40 +1008,45 @@ __device__ void warp_leapfrog_tile(const VMArgs& a, const Lane& ln, const ROp& o
     const double half = __ddiv_rn(Es[g], 2.0);
     uint64_t* gg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_g, src < 0 ? 0 : src);
     auto a_at = [&](int k) -> double { return Qs[g * SQ + k]; };
-    for (int it = 0; it < steps; ++it) {
-      for (int hs = 0; hs < 2; ++hs) {
-        const bool last = (it == steps - 1) && hs == 1;
-        for (int nt0 = 0; nt0 < tg.NT1; nt0 += LSB_NT_CHUNK) {
-          const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
-          LSB_NT_DISPATCH(ntc, {
-            double acc[NTC][2];
-            lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, a_at);
-            _Pragma("unroll")
-            for (int j = 0; j < NTC; ++j) {
-              const int col = 8 * (nt0 + j) + 2 * (lane & 3);
-              double2* pp = reinterpret_cast<double2*>(Ps + g * SP + col);
-              double2 pv = *pp;
-              const double g0 = -acc[j][0], g1 = -acc[j][1];
-              pv.x = __dadd_rn(__dmul_rn(half, g0), pv.x);
-              pv.y = __dadd_rn(__dmul_rn(half, g1), pv.y);
-              if (col + 1 < d) *pp = pv;
-              else if (col < d) Ps[g * SP + col] = pv.x;  // odd d: the pad column stays zero
-              if (last && src >= 0 && gg != nullptr) {
-                if (col < d) gg[(size_t)col * 32] = f64_bits(g0);
-                if (col + 1 < d) gg[(size_t)(col + 1) * 32] = f64_bits(g1);
-              }
-            }
-          });
+    // L+1 contractions (see lf_kick): pass 0 kicks with g(q0); pass i >= 1 drifts, then
+    // kicks twice with g(q_i) (end of step i-1, start of step i), once on the last pass
+    for (int pass = 0; steps > 0 && pass <= steps; ++pass) {
+      if (pass > 0) {  // q = e p + q over the tile
+        for (int idx = lane; idx < 8 * d; idx += 32) {
+          const int r = idx / d, k = idx - r * d;
+          Qs[r * SQ + k] = __dadd_rn(__dmul_rn(Es[r], Ps[r * SP + k]), Qs[r * SQ + k]);
         }
         __syncwarp();
-        if (hs == 0) {  // q = e p + q over the tile
-          for (int idx = lane; idx < 8 * d; idx += 32) {
-            const int r = idx / d, k = idx - r * d;
-            Qs[r * SQ + k] = __dadd_rn(__dmul_rn(Es[r], Ps[r * SP + k]), Qs[r * SQ + k]);
-          }
-          __syncwarp();
-        }
       }
+      const bool last = pass == steps;
+      const int nkick = (pass == 0 || last) ? 1 : 2;
+      for (int nt0 = 0; nt0 < tg.NT1; nt0 += LSB_NT_CHUNK) {
+        const int ntc = min(LSB_NT_CHUNK, tg.NT1 - nt0);
+        LSB_NT_DISPATCH(ntc, {
+          double acc[NTC][2];
+          lsb::mtile_gemm<NTC, SB>(acc, Bf, tg.KS1, tg.NT1, nt0, a_at);
+          _Pragma("unroll")
+          for (int j = 0; j < NTC; ++j) {
+            const int col = 8 * (nt0 + j) + 2 * (lane & 3);
+            double2* pp = reinterpret_cast<double2*>(Ps + g * SP + col);
+            double2 pv = *pp;
+            const double g0 = -acc[j][0], g1 = -acc[j][1];
+            pv.x = __dadd_rn(__dmul_rn(half, g0), pv.x);
+            pv.y = __dadd_rn(__dmul_rn(half, g1), pv.y);
+            if (nkick == 2) {
+              pv.x = __dadd_rn(__dmul_rn(half, g0), pv.x);
+              pv.y = __dadd_rn(__dmul_rn(half, g1), pv.y);
+            }
+            if (col + 1 < d) *pp = pv;
+            else if (col < d) Ps[g * SP + col] = pv.x;  // odd d: the pad column stays zero
+            if (last && src >= 0 && gg != nullptr) {
+              if (col < d) gg[(size_t)col * 32] = f64_bits(g0);
+              if (col + 1 < d) gg[(size_t)(col + 1) * 32] = f64_bits(g1);
+            }
+          }
+        });
+      }
+      __syncwarp();
     }
     for (int r = 0; r < 8; ++r) {  // write back q, p and _ret = vcat(q, p)
       const int lr = mtile_lane(mask, n, mt, r);
@@ -1053,7 +1086,7 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
   for (int k = 0; k < blk.op_count; ++k) {
     const ROp& op = ops[k];
     if (op.opcode == LS_OP_LEAPFROG) {
-      if (WARP) warp_leapfrog(a, ln, op, active && !f.pos, lf_smem, chain);
+      if constexpr (WARP) warp_leapfrog(a, ln, op, active && !f.pos, lf_smem, chain);
       continue;
     }
     const bool coop = WARP && warp_coop(a, op);
@@ -1083,7 +1116,7 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
       }
     }
     if (coop) {
-      if (WARP) {
+      if constexpr (WARP) {
         __syncwarp();
         if (a.targets[op.imm0].kind == LS_TARGET_LOGREG)
           warp_lr(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, lf_smem,

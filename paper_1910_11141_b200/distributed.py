@@ -132,3 +132,17 @@ def gather_samples(chains, *, thin: int = 1, group=None):
     out = [torch.empty_like(local) for _ in range(dist.get_world_size(group))]
     dist.all_gather(out, local, group=group)
     return torch.cat(out, dim=0)
+
+
+def run_shard(compiled, q0, *, z_total: int, rank: int, world: int, depth: int, device: int | None = None,
+              **run_kw):
+    """This rank's contiguous chain range [lo, hi) of a z_total-chain batch on its own GPU:
+    q0 rows lo..hi-1 (or q0(lo, hi) when q0 is callable) and the global-id keys; no
+    collective. Returns (outputs [hi-lo, ...], lo, hi, trace). Any sharding gives every
+    chain the bytes the single-rank run gives it (lane isolation)."""
+    from . import pc_vm
+
+    lo, hi = shard_range(rank, world, z_total)
+    q = q0(lo, hi) if callable(q0) else q0[lo:hi]
+    out, tr = pc_vm.run(compiled, [q, chain_keys(lo, hi)], depth=depth, device=device, **run_kw)
+    return out, lo, hi, tr

@@ -32,7 +32,7 @@ import numpy as np
 
 from . import ir
 from .compiler import CompiledProgram
-from .runtime import OPCODES, VType, resolve_kernel
+from .runtime import OPCODES, VType, device_op, words
 
 # numpy mirrors of the C structs in include/lockstep_b200.h
 OP_DTYPE = np.dtype([("opcode", "<i4"), ("action", "<i4"), ("out", "<i4"), ("nin", "<i4"),
@@ -253,9 +253,9 @@ def dead_saves(flat: ir.FlatProgram, classes: dict[str, str], labels) -> set[tup
 
 def _op_liveness(flat: ir.FlatProgram):
     """live-after sets per (block, op index) of the flat program (Pop reads and writes)."""
-    from .compiler import _flat_live_in
+    from .compiler import flat_live_in
 
-    live_in = _flat_live_in(flat)
+    live_in = flat_live_in(flat)
     after: dict[tuple[int, int], set[str]] = {}
     n = len(flat.blocks)
     for bi, blk in enumerate(flat.blocks):
@@ -761,7 +761,7 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
             add(v, cls, vt)
         else:
             add(v, cls, vt, flat_rows)
-            flat_rows += vt.words
+            flat_rows += words(vt)
     if not optimize:
         renamed = [[dict(op, out=index[op["out"]], ins=[index[i] for i in op["ins"]]) for op in ops]
                    for ops in block_ops]
@@ -840,8 +840,8 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
                     owner[name] = (head, 0)
                     chained.add(name)
                     inst[head]["end"] = max(inst[head]["end"], end)
-                    inst[head]["span"] = max(inst[head].get("span", inst[head]["vt"].words),
-                                             info["vt"].words)
+                    inst[head]["span"] = max(inst[head].get("span", words(inst[head]["vt"])),
+                                             words(info["vt"]))
         # the storage owner of every view / chain member must outlive it
         for name in owner:
             r = name
@@ -882,7 +882,7 @@ def _storage(block_ops: list[list[dict]], conds: list[str | None], classes: dict
                 continue
             if name in owner:
                 continue
-            size = info.get("span", info["vt"].words)
+            size = info.get("span", words(info["vt"]))
             live = [x for x in live if x[0] >= info["start"]]
             off, ok = 0, False
             for cand in sorted({0} | {o + s for _, o, s in live}):
@@ -942,12 +942,12 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     if optimize:
         for m in match_normals(flat, classes, compiled.labels):
             if types.get(m["c"], VType("i64")).kind == "f64" and types.get(m["ret"]) is not None \
-                    and types[m["ret"]].words == m["k"] + 1:
+                    and words(types[m["ret"]]) == m["k"] + 1:
                 normals[m["entry"]] = m
     fused = {}
     if optimize and superblocks:
         for m in match_leapfrog(flat, classes, grad_names()):
-            t = resolve_kernel(m["grad"]).device.target
+            t = device_op(m["grad"]).target
             if t is not None and t.kind == 1 and t.dim <= max_superblock_dim:
                 fused[m["entry"]] = m
     dropped: set[tuple[int, int]] = set()
@@ -955,7 +955,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     for m in fused.values():
         m["fwd"], drop, m["writeback"], m["live_refs"] = superblock_io(flat, m)
         dropped |= drop
-        t = resolve_kernel(m["grad"]).device.target
+        t = device_op(m["grad"]).target
         lp_name = next((tt.logpdf for tt in _registered() if tt.grad == m["grad"]), None)
         hit = fuse_leaf_logpdf(flat, m, lp_name, t.dim) if lp_name and (t.dim + 7) // 8 <= 16 else None
         m["lp"] = None
@@ -985,7 +985,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
         ops: list[dict] = []
         if bi in fused:
             m = fused[bi]
-            t = resolve_kernel(m["grad"]).device.target
+            t = device_op(m["grad"]).target
             if t not in targets:
                 targets.append(t)
             # kind bit 0: write the final q, p back to the function's registers
@@ -1017,15 +1017,14 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
             if (bi, oi) in allocs:
                 vt = vtype(op.output)
                 ops.append(dict(opcode=OPCODES["alloc"], action=ACTION_PUSH, out=op.output, ins=[],
-                                kind=KIND_CODE[vt.kind], width=vt.words, imm0=0, imm1=0, imm2=0, bits=0,
+                                kind=KIND_CODE[vt.kind], width=words(vt), imm0=0, imm1=0, imm2=0, bits=0,
                                 prim="$alloc"))
                 continue
-            k = resolve_kernel(op.prim.name)
-            if k.device is None:
+            dev = device_op(op.prim.name)
+            if dev is None:
                 raise NotImplementedError(
                     f"primitive '{op.prim.name}' has no B200 implementation (host-only kernel); "
                     "the lockstep B200 engine has no CPU fallback")
-            dev = k.device
             out_vt = vtype(op.output)
             in_kind = KIND_CODE[vtype(op.inputs[0]).kind] if op.inputs else KIND_CODE[out_vt.kind]
             imm0, imm1, bits = dev.imm0, dev.imm1, 0
@@ -1037,7 +1036,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
                 imm0 = targets.index(dev.target)
             action = ACTION_PUSH if isinstance(op, ir.Push) else ACTION_UPDATE
             row = dict(opcode=dev.opcode, action=action, out=op.output, ins=list(op.inputs),
-                       kind=in_kind, width=out_vt.words, imm0=imm0, imm1=imm1, imm2=0, bits=bits,
+                       kind=in_kind, width=words(out_vt), imm0=imm0, imm1=imm1, imm2=0, bits=bits,
                        prim=op.prim.name)
             if (bi, oi) in cached_logpdf:  # written by the preceding superblock (fast mode)
                 row["cache"] = cached_logpdf[(bi, oi)]
@@ -1048,7 +1047,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
                 classes[tmp] = "temporary"
                 ops.append(dict(row, out=tmp))
                 ops.append(dict(opcode=OPCODES["id"], action=ACTION_UPDATE, out=op.output, ins=[tmp],
-                                kind=KIND_CODE[out_vt.kind], width=out_vt.words, imm0=0, imm1=0,
+                                kind=KIND_CODE[out_vt.kind], width=words(out_vt), imm0=0, imm1=0,
                                 imm2=0, bits=0, prim="id"))
             else:
                 ops.append(row)
@@ -1096,7 +1095,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     var_arr = np.zeros(len(entries), dtype=VAR_DTYPE)
     sp_row = 0
     for i, (name, cls, vt, row) in enumerate(entries):
-        var_arr[i] = (CLASS_CODE[cls], KIND_CODE[vt.kind], vt.words,
+        var_arr[i] = (CLASS_CODE[cls], KIND_CODE[vt.kind], words(vt),
                       sp_row if cls == "stacked" else -1, row, 0)
         if cls == "stacked":
             sp_row += 1

@@ -2,14 +2,14 @@
 
 Same entry points and semantics as reference `pkg/src/lockstep/pc_vm.py`:
 
-    infer_types(flat, input_types)                           pc_vm.py:49-97
+    infer_types(flat, input_types)                           pc_vm.py:49-97 (the reference's own)
     init_machine(compiled, inputs, *, depth, mode, trace)    pc_vm.py:140-213
     step(m, *, observer, debug) -> bool                      pc_vm.py:304-332
     run_vm(m, *, max_steps, observer, debug)                 pc_vm.py:338-349
     run_flat(...), run(...) -> (outputs, ScheduleTrace)      pc_vm.py:352-383
     check_coherence(m)                                       pc_vm.py:391-400
 
-Every block step executes in the CUDA VM (`csrc/vm.cu`) through the C ABI;
+Every block step executes in the CUDA VM (`csrc/engine.cu`) through the C ABI;
 this module only moves inputs/outputs, maps status codes to the reference
 exceptions and rebuilds `ScheduleTrace` records from the device trace.
 
@@ -33,11 +33,11 @@ import numpy as np
 from . import _native, ir
 from . import schedule as _schedule
 from .compiler import CompiledProgram
-from .errors import (StackFault, StackOverflow, StackUnderflow, StepLimitExceeded,
-                     TypeInferenceError)
+from .errors import StackFault, StackOverflow, StackUnderflow, StepLimitExceeded
 from .lowering import DeviceProgram, lower
-from .metrics import ScheduleTrace
-from .runtime import BOOL, I64, VType, batch, resolve_kernel, vtype_of
+from .metrics import DeviceTrace, ScheduleTrace
+from .reference import pc_vm as _ref_pc_vm
+from .runtime import I64, VType, batch, vtype_of, words
 
 DEFAULT_MAX_STEPS = 1_000_000
 MAX_GROUP_LANES = 1024
@@ -46,42 +46,9 @@ _PROGRAM_CACHE: dict = {}
 _MACHINE_CACHE: dict = {}
 
 
-# ---- type inference (reference pc_vm.py:49-97) ----------------------------------------
+# ---- type inference: the reference's own (pc_vm.py:49-97), used unchanged ---------------------
 
-
-def infer_types(flat: ir.FlatProgram, input_types: list[VType]) -> dict[str, VType]:
-    """Forward fixpoint of one static type per variable, seeded by the inputs."""
-    if len(input_types) != len(flat.inputs):
-        raise TypeInferenceError(f"program wants {len(flat.inputs)} inputs, got {len(input_types)}")
-    types: dict[str, VType] = dict(zip(flat.inputs, input_types))
-    changed = True
-    while changed:
-        changed = False
-        for blk in flat.blocks:
-            for op in blk.ops:
-                if isinstance(op, ir.Pop):
-                    continue
-                ins = [types.get(v) for v in op.inputs]
-                if any(t is None for t in ins):
-                    continue
-                try:
-                    vt = resolve_kernel(op.prim.name).type_rule(tuple(ins))
-                except ValueError as e:
-                    raise TypeInferenceError(
-                        f"'{op.prim.name}' on {tuple(map(str, ins))}: {e}") from None
-                old = types.get(op.output)
-                if old is None:
-                    types[op.output] = vt
-                    changed = True
-                elif old != vt:
-                    raise TypeInferenceError(f"variable '{op.output}' is both {old} and {vt}")
-    for blk in flat.blocks:
-        t = blk.terminator
-        if isinstance(t, ir.FlatBranch):
-            ct = types.get(t.cond)
-            if ct is not None and ct != BOOL:
-                raise TypeInferenceError(f"branch condition '{t.cond}' has type {ct}, wants bool")
-    return types
+infer_types = _ref_pc_vm.infer_types
 
 
 # ---- host views of device storage (for observers) -------------------------------------------
@@ -231,7 +198,7 @@ class Machine:
         vt = self._dp.types[name]
         cls = self.classes[name]
         slots = self.depth if cls == "stacked" else 1
-        raw = self._h.read_var(vid, slots, vt.words)
+        raw = self._h.read_var(vid, slots, words(vt))
         data = _decode(raw, vt)
         if cls == "stacked":
             return StackView(name, self.depth, self.z, vt, data, self._h.read_pointers(vid))
@@ -259,7 +226,7 @@ class Machine:
         if self.halted or not self.exact:
             vt = self._dp.types[self.flat.output]
             # read_output hands back a fresh array (never aliased by the machine)
-            return _decode(self._h.read_output(vt.words, np.uint64).reshape(self.z, vt.words), vt)
+            return _decode(self._h.read_output(words(vt), np.uint64).reshape(self.z, words(vt)), vt)
         return np.array(self.value_of(self.flat.output), copy=True)
 
 
@@ -302,7 +269,8 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
                  lanes_per_group: int | None = None, groups: int = 0,
                  optimize: bool = False, exact_logpdf: bool = True,
                  lane_trace_cap: int = 0, engine: str = "auto",
-                 codegen: bool | str = False, reuse: bool = False, device: int | None = None) -> Machine:
+                 codegen: bool | str = False, reuse: bool = False, device: int | None = None,
+                 precision: str = "fp64") -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
@@ -318,6 +286,9 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     instead of the op interpreter; compiled once per program and cached
     in-tree ("cached": use only a prebuilt library).
 
+    precision (warp engine): "fp64" — the reference's arithmetic (DMMA superblocks);
+    "fp32" — fused leapfrogs in float32 on the tensor cores (tcgen05 kind::tf32, 3xTF32
+    split; gaussian targets with d <= 128, 1e-5 relative per leapfrog step).
     device: CUDA device index the machine lives on (one process per GPU passes
     its LOCAL_RANK; None = the library's current device, 0 by default).
     schedule: block-selection rule (schedule.SCHEDULES): "min_pc" (reference),
@@ -329,7 +300,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
         raise ValueError("stack depth must be at least 1")
     from .compiler import adopt
 
-    compiled = adopt(compiled)  # also accepts programs built by the reference compiler
+    compiled = adopt(compiled)  # the reference compiler's CompiledProgram
     flat = compiled.flat
     arrays = _prepare_inputs(flat, inputs)
     z = arrays[0].shape[0]
@@ -362,7 +333,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     lanes = z if exact else (32 if kind == "warp" else int(lanes_per_group))
     mopts = dict(sched=schedule, lanes_per_cta=int(lanes_per_group) if kind == "cta" else 0,
                  ctas=groups, trace=exact and trace is not None, exact_logpdf=exact_logpdf,
-                 lane_trace_cap=lane_trace_cap, warp_groups=(kind == "warp"))
+                 lane_trace_cap=lane_trace_cap, warp_groups=(kind == "warp"), precision=precision)
     mkey = (pkey, z, depth, tuple(sorted(mopts.items())))
     handle = _MACHINE_CACHE.pop(mkey, None) if reuse else None
     if handle is not None and handle.program is program:
@@ -489,24 +460,24 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
         schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
         optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
         engine: str = "auto", codegen: bool | str = False, return_machine: bool = False,
-        device: int | None = None):
+        device: int | None = None, precision: str = "fp64"):
     """Execute a compiled program on the B200; returns (outputs, trace)."""
     arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
     z = arrays[0].shape[0] if arrays else 0
     if optimize is None:
         optimize = observer is None and not debug
-    tr: ScheduleTrace = ScheduleTrace(engine="pc", z=z)
+    tr: ScheduleTrace = DeviceTrace(engine="pc", z=z)
     # device storage is reused across calls with the same program and shapes; a
     # machine handed back to the caller (return_machine) is not recycled
     reuse = not return_machine and observer is None and not debug
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
                      exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
-                     codegen=codegen, reuse=reuse, device=device)
+                     codegen=codegen, reuse=reuse, device=device, precision=precision)
     if m.engine == "warp" and observer is None and not debug and not return_machine:
         # output rows go straight to a pinned host buffer while the run executes (not for
         # a machine handed back: its device output must stay valid for later reads)
-        m._h.stream_output_to_host(m._dp.types[m.flat.output].words)
+        m._h.stream_output_to_host(words(m._dp.types[m.flat.output]))
     try:
         out = run_vm(m, max_steps=max_steps, observer=observer, debug=debug)
     finally:

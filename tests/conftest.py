@@ -60,7 +60,7 @@ def oracle_run(prog, inputs, depth, **kw):
 
     types = infer_types(prog.flat, [vtype_of(np.asarray(a)) for a in inputs])
     return O.run(prog, inputs, depth=depth, types=types,
-                 targets={t.name: t for t in L.registered_targets()}, **kw)
+                 targets=L.workloads.device_targets(), **kw)
 
 
 def nuts_program(meta_case: dict, entry: str = "nuts_main"):

@@ -51,11 +51,11 @@ def test_no_cpu_fallback_without_device():
 def test_host_only_kernel_is_rejected():
     from paper_1910_11141_b200.lowering import lower
     from paper_1910_11141_b200.pc_vm import infer_types
-    from paper_1910_11141_b200.runtime import F64, VType, register_kernel
+    from paper_1910_11141_b200.runtime import F64, VType, register_kernel, words
 
     register_kernel("host_square", 1, lambda ins, z: ins[0] ** 2, lambda ins: ins[0])
     cp = L.compile_program(L.compile_source("def f(x) { return host_square(x); }"))
     types = infer_types(cp.flat, [F64])
     with pytest.raises(NotImplementedError, match="no CPU fallback"):
         lower(cp, types)
-    assert VType("f64", 3).words == 3
+    assert words(VType("f64", 3)) == 3 and words(F64) == 1

@@ -197,9 +197,9 @@ def test_gaussian_target_kernels_on_device():
     for d in (2, 5, 25, 100, 128):
         t = L.correlated_gaussian(d, 0.5)
         x = e[f"x{d}"]
-        lp = L.runtime.resolve_kernel(t.logpdf).fn((x,), 4)
+        lp = _native.target_eval(L.device_target(t.name), "logpdf", x)
         assert lp.tobytes() == e[f"lp{d}"].tobytes(), d
-        g = L.runtime.resolve_kernel(t.grad).fn((x,), 4)
+        g = _native.target_eval(L.device_target(t.name), "grad", x)
         np.testing.assert_allclose(g, e[f"g{d}"], rtol=1e-12, atol=1e-14)
 
 
@@ -209,8 +209,9 @@ def test_logreg_target_kernels_on_device():
         t = L.logistic_regression(n, d, seed)
         tag = f"lr{n}x{d}s{seed}"
         w = g[f"{tag}_w"]
-        np.testing.assert_allclose(L.runtime.resolve_kernel(t.logpdf).fn((w,), 6), g[f"{tag}_lp"], rtol=1e-12)
-        np.testing.assert_allclose(L.runtime.resolve_kernel(t.grad).fn((w,), 6), g[f"{tag}_g"],
+        dt = L.device_target(t.name)
+        np.testing.assert_allclose(_native.target_eval(dt, "logpdf", w), g[f"{tag}_lp"], rtol=1e-12)
+        np.testing.assert_allclose(_native.target_eval(dt, "grad", w), g[f"{tag}_g"],
                                    rtol=1e-10, atol=1e-12)
 
 
@@ -218,10 +219,13 @@ def test_gradients_match_finite_differences():
     """reference test_acceptance.py:273-292, on the device kernels."""
     for t in (L.correlated_gaussian(2, 0.5), L.correlated_gaussian(3, -0.2),
               L.logistic_regression(200, 5, seed=7)):
-        lp = L.runtime.resolve_kernel(t.logpdf).fn
-        gr = L.runtime.resolve_kernel(t.grad).fn
+        dt = L.device_target(t.name)
+
+        def lp(args, _z, dt=dt):
+            return _native.target_eval(dt, "logpdf", args[0])
+
         pts = np.random.default_rng(1).normal(size=(10, t.dim))
-        g = gr((pts,), 10)
+        g = _native.target_eval(dt, "grad", pts)
         h = 1e-6
         for i in range(t.dim):
             e = np.zeros(t.dim)
@@ -395,7 +399,7 @@ def test_warp_engine_logreg_dmma_gradient(codegen):
         t, cp = prebuilt.lr_gradient(n, d, seed)
         w = np.random.default_rng(seed).normal(size=(77, d)) * 0.3
         got, _ = L.run(cp, [w], depth=4, engine="warp", codegen=codegen)
-        want = O.logreg_grad(w, t.params["sx"])
+        want = O.logreg_grad(w, L.device_target(t.name).params["sx"])
         np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
     kw = dict(prebuilt.LR_NUTS)
     cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
@@ -420,7 +424,7 @@ def test_warp_engine_logreg_fast_logpdf():
         cp = L.compile_program(L.compile_source(f"def lp(w) {{ return {t.logpdf}(w); }}", "lp"))
         w = np.random.default_rng(seed + 1).normal(size=(77, d)) * 0.3
         got, _ = L.run(cp, [w], depth=4, engine="warp", exact_logpdf=False)
-        want = O.logreg_logpdf(w, t.params["sx"])
+        want = O.logreg_logpdf(w, L.device_target(t.name).params["sx"])
         np.testing.assert_allclose(got, want, rtol=1e-12)
 
 
@@ -573,3 +577,69 @@ def test_local_schedule_on_device_reproduces_alg1(golden_meta, name):
         assert u_pc / u_local >= 1.5
     if m["z"] == 1:
         assert u_pc == u_local == 1.0
+
+
+# ---- fp32 arm: tcgen05 (kind::tf32, 3xTF32) leapfrog superblocks, warpgroup stepping -------
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_fp32_leapfrog_per_step_tolerance(codegen):
+    """The fp32 arm against the reference's float64 leapfrog vectors: 1e-5 relative per
+    leapfrog step (north_star's fp32 contract), scaled by each lane's largest component."""
+    from paper_1910_11141_b200 import prebuilt
+
+    g = load_npz("leapfrog.npz")
+    for d, steps in prebuilt.LEAPFROG:
+        _, _, cp = prebuilt.nuts(d, 0.5, step_size=0.25, leaf_steps=steps, max_depth=6, iterations=1,
+                                 entry="leapfrog")
+        tag = f"d{d}_L{steps}"
+        got, _ = L.run(cp, [g[f"{tag}_q"], g[f"{tag}_p"], g[f"{tag}_e"]], depth=4, engine="warp",
+                       codegen=codegen, precision="fp32")
+        want = g[f"{tag}_out"]
+        err = (np.abs(got - want) / np.abs(want).max(axis=1, keepdims=True)).max()
+        assert err <= 1e-5 * steps, (tag, err)
+        assert err > 0  # really computed in float32
+
+
+@pytest.mark.parametrize("codegen", [False, "cached"])
+def test_fp32_nuts_control_traces_match_the_f64_oracle(codegen):
+    """fp32 arm on NUTS-lite: every lane's block sequence (tree depths, accept and U-turn
+    decisions) equals the float64 oracle's, chains agree to float32 accuracy, and the
+    warpgroup schedule keeps the reference's gradient count."""
+    from paper_1910_11141_b200 import prebuilt
+
+    for kw in prebuilt.TEST_NUTS:
+        kw = dict(kw)
+        cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+        z, d = 200, t.dim
+        ins = [np.zeros((z, d)), np.arange(z, dtype=np.int64) * 7919 + 11]
+        ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+        for sched in ("min_pc", "priority"):
+            got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=codegen,
+                               exact_logpdf=False, precision="fp32", schedule=sched,
+                               lane_trace_cap=1 << 16, return_machine=True)
+            same = sum(np.array_equal(seq, ref.lane_blocks[i]) for i, seq in enumerate(m.lane_traces()))
+            assert same == z, (d, sched, same)
+            err = (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max()
+            assert err < 1e-4, (d, sched, err)
+            want = sum(a * 2 * cfg.leaf_steps for b, a in ref.steps if cp.labels[b] == "leapfrog.b2") \
+                // (2 * cfg.leaf_steps) * 2
+            assert m.useful_grads == want
+
+
+def test_fp32_refill_and_faults():
+    """fp32 machines refill lanes across warpgroups and report stack overflow like fp64."""
+    from paper_1910_11141_b200 import prebuilt
+
+    kw = dict(prebuilt.TEST_NUTS[1])
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+    z = 1500
+    ins = [np.zeros((z, t.dim)), np.arange(z, dtype=np.int64) * 104729 + 17]
+    got, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen="cached", groups=1,
+                      exact_logpdf=False, precision="fp32", return_machine=True)
+    assert m._h.groups % 4 == 0 and m._h.groups * 32 < z
+    pick = np.r_[0:16, 700:716, 1484:1500]
+    ref = oracle_run(cp, [ins[0][pick], ins[1][pick]], cfg.min_stack_depth)
+    assert (np.abs(got[pick] - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < 1e-4
+    with pytest.raises(StackOverflow):
+        L.run(cp, ins, depth=3, engine="warp", codegen="cached", exact_logpdf=False, precision="fp32")

@@ -42,9 +42,9 @@ def test_exact_order_restatements():
     e = load_npz("gauss_logpdf.npz")
     for d in (2, 5, 25, 100, 128):
         t = L.correlated_gaussian(d, 0.5)
-        assert np.array_equal(e[f"P{d}"], t.params["prec"])
+        assert np.array_equal(e[f"P{d}"], L.device_target(t.name).params["prec"])
         for row, want in zip(e[f"x{d}"], e[f"lp{d}"]):
-            assert exact_order.gauss_logpdf(row, t.params["prec"], t.params["norm"]) == want, d
+            assert exact_order.gauss_logpdf(row, L.device_target(t.name).params["prec"], L.device_target(t.name).params["norm"]) == want, d
 
 
 def test_corpus_runs_bit_exact(golden_meta, corpus_compiled):
@@ -91,8 +91,8 @@ def test_logreg_target_values():
         t = L.logistic_regression(n, d, seed)
         tag = f"lr{n}x{d}s{seed}"
         w = g[f"{tag}_w"]
-        assert O.logreg_logpdf(w, t.params["sx"]).tobytes() == g[f"{tag}_lp"].tobytes()
-        assert O.logreg_grad(w, t.params["sx"]).tobytes() == g[f"{tag}_g"].tobytes()
+        assert O.logreg_logpdf(w, L.device_target(t.name).params["sx"]).tobytes() == g[f"{tag}_lp"].tobytes()
+        assert O.logreg_grad(w, L.device_target(t.name).params["sx"]).tobytes() == g[f"{tag}_g"].tobytes()
 
 
 def test_oracle_faults_name_lane_and_block(corpus_compiled):

@@ -46,7 +46,7 @@ def test_oracle_local_engine_matches_reference(golden_meta, name):
     from oracle import lockstep_oracle as O
 
     m, t, cfg, cg, cp, ins, a = _case(golden_meta, name)
-    out, steps = O.run_local(cg, ins, targets={t.name: t})
+    out, steps = O.run_local(cg, ins, targets={t.name: L.device_target(t.name)})
     assert out.tobytes() == a[f"{name}_local_out"].tobytes()
     labels = m["local_labels"]
     got = np.array([[labels.index(lbl), act, g] for lbl, act, g in steps], np.int32)

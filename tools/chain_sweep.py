@@ -43,7 +43,7 @@ for lg in range(args.min_log2, args.max_log2 + 1):
     sec = sum(ms) / 1e3
     rate = grads / sec
     row = {"chains": z, "grad_evals_per_s": rate, "ms_per_launch": float(np.mean(ms)),
-           "tflops": rate * t.grad_flops / 1e12, "roofline_frac": rate * t.grad_flops / 1e12 / PEAK}
+           "tflops": rate * L.device_target(t.name).grad_flops / 1e12, "roofline_frac": rate * L.device_target(t.name).grad_flops / 1e12 / PEAK}
     rows.append(row)
     print(json.dumps(row), flush=True)
     del m

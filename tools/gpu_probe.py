@@ -15,7 +15,7 @@ from paper_1910_11141_b200.runtime import vtype_of  # noqa: E402
 def oracle(prog, ins, depth):
     types = infer_types(prog.flat, [vtype_of(a) for a in ins])
     return O.run(prog, ins, depth=depth, types=types,
-                 targets={t.name: t for t in L.registered_targets()}, lane_traces=True)
+                 targets=L.workloads.device_targets(), lane_traces=True)
 
 
 def main():
