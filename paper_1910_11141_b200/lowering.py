@@ -351,6 +351,57 @@ def coalesce_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatPro
     return ir.FlatProgram(tuple(blocks), flat.inputs, flat.output, flat.entry)
 
 
+def forward_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatProgram:
+    """Copy forwarding through single-use temporaries: `update T = id X; ...; update V = id T`
+    (T a temporary read only there) becomes `update V = id X` at T's position when nothing in
+    between reads or writes V, and disappears when V is X. E.g. the argument copies of
+    every call (`$a = id qp; ...; build_tree.q = id $a`): one copy instead of two, and
+    none at all for a recursive call passing its own parameter (`q = id q`)."""
+    blocks = []
+    changed = False
+    for blk in flat.blocks:
+        ops = list(blk.ops)
+        cond = blk.terminator.cond if isinstance(blk.terminator, ir.FlatBranch) else None
+        uses: dict[str, list[int]] = {}
+        defs: dict[str, list[int]] = {}
+        for k, op in enumerate(ops):
+            if isinstance(op, ir.Pop):
+                continue
+            for v in op.inputs:
+                uses.setdefault(v, []).append(k)
+            defs.setdefault(op.output, []).append(k)
+        drop: set[int] = set()
+        put: dict[int, object] = {}
+        for k2, op in enumerate(ops):
+            if not (isinstance(op, ir.Update) and op.prim.name == "id") or k2 in drop:
+                continue
+            t, v = op.inputs[0], op.output
+            if classes.get(t) != "temporary" or t == v or t == cond or uses.get(t) != [k2]:
+                continue
+            if len(defs.get(t, ())) != 1:
+                continue
+            k1 = defs[t][0]
+            src = ops[k1]
+            if k1 >= k2 or k1 in drop or k1 in put or not (isinstance(src, ir.Update) and src.prim.name == "id"):
+                continue
+            x = src.inputs[0]
+            between = ops[k1 + 1:k2]
+            if any((isinstance(o, ir.Pop) and o.var == v) or
+                   (not isinstance(o, ir.Pop) and (o.output == v or v in o.inputs)) for o in between):
+                continue
+            drop.add(k2)
+            if x == v:
+                drop.add(k1)
+            else:
+                put[k1] = ir.Update(v, src.prim, (x,))
+            changed = True
+        new_ops = [put.get(k, op) for k, op in enumerate(ops) if k not in drop]
+        blocks.append(ir.FlatBlock(tuple(new_ops), blk.terminator))
+    if not changed:
+        return flat
+    return ir.FlatProgram(tuple(blocks), flat.inputs, flat.output, flat.entry)
+
+
 def fuse_copies(flat: ir.FlatProgram, classes: dict[str, str]) -> ir.FlatProgram:
     """`update T = f(xs); update V = id T` (T temporary, single use) -> `update V = f(xs)`."""
     uses: dict[str, int] = {}
@@ -573,15 +624,13 @@ def match_normals(flat: ir.FlatProgram, classes: dict[str, str], labels) -> list
                 raise ValueError
             if pos != len(ops) or classes.get(ret.output) != "register":
                 raise ValueError
-            if fn_of[b] != key.split(".", 1)[0] or fn_of[b] != c.split(".", 1)[0]:
-                raise ValueError
         except (ValueError, AttributeError, IndexError):
             continue
         found.append(dict(entry=b, key=key, c=c, ret=ret.output, k=k, pairs=pairs))
     return found
 
 
-def superblock_io(flat: ir.FlatProgram, m: dict) -> tuple[dict, set[tuple[int, int]], int, list]:
+def superblock_io(flat: ir.FlatProgram, m: dict, classes: dict | None = None) -> tuple[dict, set[tuple[int, int]], int, list]:
     """Operand forwarding and dead side outputs of a fused leapfrog function `m`.
 
     The superblock runs immediately after its call block, so an argument copied
@@ -625,17 +674,19 @@ def superblock_io(flat: ir.FlatProgram, m: dict) -> tuple[dict, set[tuple[int, i
             a = o.inputs[0]
             adefs = [j for j, x in enumerate(ops[:k]) if not isinstance(x, ir.Pop) and x.output == a]
             uses = [j for j, x in enumerate(ops) if not isinstance(x, ir.Pop) and a in x.inputs]
-            if len(adefs) != 1 or uses != [k] or not a.split(".", 1)[-1].startswith("$a"):
+            ad = ops[adefs[0]] if len(adefs) == 1 else None
+            if (uses == [k] and a.split(".", 1)[-1].startswith("$a") and isinstance(ad, ir.Update)
+                    and ad.prim.name == "id"):
+                x, start, here = ad.inputs[0], adefs[0], {(cb, adefs[0]), (cb, k)}
+            elif (classes or {}).get(a, "temporary") != "temporary":  # param = id X (forward_copies)
+                x, start, here = a, k, {(cb, k)}
+            else:
                 break
-            ad = ops[adefs[0]]
-            if not (isinstance(ad, ir.Update) and ad.prim.name == "id"):
-                break
-            x = ad.inputs[0]
             if any((isinstance(y, ir.Pop) and y.var == x) or (not isinstance(y, ir.Pop) and y.output == x)
-                   for y in ops[adefs[0] + 1:]):
+                   for y in ops[start + 1:]):
                 break
             srcs.add(x)
-            pos |= {(cb, adefs[0]), (cb, k)}
+            pos |= here
         else:
             if len(srcs) == 1:
                 fwd[param] = srcs.pop()
@@ -936,6 +987,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
         flat, classes = demote_nonreentrant(flat, classes, compiled.labels)
         flat, classes = demote_unpushed(flat, classes)
         flat = fuse_copies(flat, classes)
+        flat = forward_copies(flat, classes)
         flat = coalesce_copies(flat, classes)
         allocs = dead_saves(flat, classes, compiled.labels)
     normals = {}
@@ -953,7 +1005,7 @@ def lower(compiled: CompiledProgram, types: dict[str, VType], *, optimize: bool 
     dropped: set[tuple[int, int]] = set()
     cached_logpdf: dict[tuple[int, int], str] = {}
     for m in fused.values():
-        m["fwd"], drop, m["writeback"], m["live_refs"] = superblock_io(flat, m)
+        m["fwd"], drop, m["writeback"], m["live_refs"] = superblock_io(flat, m, classes)
         dropped |= drop
         t = device_op(m["grad"]).target
         lp_name = next((tt.logpdf for tt in _registered() if tt.grad == m["grad"]), None)
