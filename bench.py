@@ -69,6 +69,7 @@ def parse():
     ap.add_argument("--cpu-chains", type=int, default=256)
     ap.add_argument("--no-sweep", action="store_true", help="skip the 2^10..2^20 chain sweep")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 (tcgen05) arm")
+    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 3 and 5")
     ap.add_argument("--cpu-iterations", type=int, default=10)
     return ap.parse_args()
 
@@ -183,6 +184,18 @@ def flush_l2(torch, dev):
     buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     buf.fill_(1)
     torch.cuda.synchronize(dev)
+
+
+def measured_traffic(lib) -> dict | None:
+    """DRAM bytes per launch of this very library (by content hash) from an `ncu --set full`
+    capture of the same command, recorded in profiles/traffic.json; None if not captured."""
+    if lib is None:
+        return None
+    try:
+        table = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    return table.get(os.path.basename(str(lib)))
 
 
 def measured_peaks() -> dict:
@@ -404,12 +417,18 @@ def main():
 
     # roofline of the dominant kernel (vm_kernel: the whole step is one launch)
     flops_per_grad = L.device_target(target.name).grad_flops
+    args_leaf_steps = cfg.leaf_steps  # the superblock executes L+1 of the 2L reference gradients
     achieved = (grads / args.steps) * flops_per_grad / (np.mean(times) / 1e3) / 1e12
+    traffic = measured_traffic(lib)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_FALLBACK, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_FALLBACK, "traffic": None,
-                "note": ("fp64 gradient FLOPs (2*d^2 per useful grad) / vm_kernel launch time; "
-                         "peak = measured fp64 DFMA/DMMA rate (tools/fp64_peaks.cu), MEASURED_PEAKS.json "
-                         "has no fp64 figure")}
+                "frac": achieved / FP64_PEAK_FALLBACK,
+                "traffic": traffic["bytes_per_launch"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else "no ncu capture of this library",
+                "executed_frac": achieved / FP64_PEAK_FALLBACK * (args_leaf_steps + 1) / (2 * args_leaf_steps),
+                "note": ("fp64 gradient FLOPs (2*d^2 per useful, reference-equivalent grad: 2L per leaf) / "
+                         "vm_kernel launch time; executed_frac counts the L+1 contractions per leaf the fused "
+                         "superblock performs; peak = measured fp64 DFMA/DMMA rate (tools/fp64_peaks.cu), "
+                         "MEASURED_PEAKS.json has no fp64 figure")}
 
     # e2e through the public API with host buffers (H2D of inputs, D2H of chains inside)
     e2e = None
@@ -498,6 +517,41 @@ def main():
                 sweep[precision].append({"chains": zz, "value": v, "ms": ms,
                                          "frac": v * flops_per_grad / 1e12 / peak})
 
+    # BASELINE configs 3 and 5 (one warm + one timed launch each, fp64, same engine/schedule)
+    configs = None
+    if rank == 0 and world == 1 and warp and not args.no_configs:
+        configs = {}
+        from paper_1910_11141_b200 import prebuilt
+
+        def cfg_point(label, cfgx, tx, cpx, zz, inputs_fn):
+            dtx = L.device_target(tx.name)
+            m2 = L.init_machine(cpx, inputs_fn(zz), depth=cfgx.min_stack_depth, engine="warp", optimize=True,
+                                exact_logpdf=False, codegen="cached", schedule=args.schedule)
+            m2._h.run(-1)
+            m2._h.reset()
+            flush_l2(torch, dev)
+            st2 = m2._h.run(-1)
+            v = st2.useful_grads / (st2.kernel_ms / 1e3)
+            configs[label] = {"chains": zz, "iterations": cfgx.iterations, "max_tree_depth": cfgx.max_depth,
+                              "step_size": cfgx.step_size, "value": v, "unit": UNIT, "ms": st2.kernel_ms,
+                              "useful_grads": int(st2.useful_grads), "flops_per_grad": dtx.grad_flops,
+                              "frac": v * dtx.grad_flops / 1e12 / FP64_PEAK_FALLBACK, "precision": "fp64"}
+
+        kw = dict(prebuilt.CONFIG3)
+        c3, t3, cp3 = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+        cfg_point("config3_logreg_1000x25", c3, t3, cp3, 1 << 16,
+                  lambda zz: [np.zeros((zz, t3.dim)), chain_keys(0, zz)])
+        kw = dict(prebuilt.DISPERSED)
+        cd, td, cpd = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+        cfg_point("dispersed_init_gauss100_eps0.1", cd, td, cpd, 1 << 16,
+                  lambda zz: [np.random.default_rng(1).standard_normal((zz, td.dim)), chain_keys(0, zz)])
+        configs["dispersed_init_gauss100_eps0.1"]["note"] = (
+            "headline target, q0 ~ N(0, I) per chain, step 0.1: tree depths vary across chains")
+        kw = dict(prebuilt.CONFIG5)
+        c5, t5, cp5 = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+        cfg_point("config5_gauss1000_cond1e4_depth15", c5, t5, cp5, 1 << 11,
+                  lambda zz: [np.zeros((zz, t5.dim)), chain_keys(0, zz)])
+
     # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)
     from paper_1910_11141_b200.distributed import diagnostics
 
@@ -520,6 +574,7 @@ def main():
             "config": {**workload_config(args, target), "parallelism": f"chains sharded over {world} GPU(s)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "diagnostics": diag_summary, "parity": parity, "fp32": fp32, "sweep": sweep,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -175,8 +175,9 @@ typedef struct {
 
 /* ls_machine_opts.flags */
 #define LS_MF_FP32 2      /* warp engine, fp32 arm: fused leapfrogs in float32 on the tensor cores
-                             (tcgen05 kind::tf32, 3xTF32 split), the 4 warps of a warpgroup
-                             stepping together (gaussian targets, d <= 128, keyed schedules) */
+                             (tcgen05 kind::tf32, 3xTF32 split); the warps of a warpgroup meet
+                             at each superblock and contract their chains together (gaussian
+                             targets, d <= 128) */
 #define LS_MF_NO_STAGE 1  /* warp engine: read target matrices from global memory
                              instead of a per-CTA shared-memory copy */
 

@@ -50,6 +50,10 @@ OPT = {"noalias": os.environ.get("LSB_CG_NOALIAS", "0") == "1",
        "ewu": int(os.environ.get("LSB_CG_EWU", "16")),
        # dev-only superblock phase clocks (tools/sb_profile.py)
        "sbprof": int(os.environ.get("LSB_CG_SBPROF", "0")),
+       # blocks with identical code on different variables share warp steps (find_pairs)
+       "pairs": int(os.environ.get("LSB_CG_PAIRS", "1")),
+       # warps per CTA of the warp engine (registers per thread = 65536 / (32 * wmax))
+       "wmax": int(os.environ.get("LSB_CG_WMAX", "16")),
        # dev-only per-block SM-cycle accounting (clock64 + atomics; tools/block_profile.py)
        "bprof": int(os.environ.get("LSB_CG_BPROF", "0")),
        # n-tiles per superblock kick pass
@@ -85,6 +89,7 @@ def _u64(bits: int) -> str:
 class _Gen:
     def __init__(self, dp: DeviceProgram):
         self.dp = dp
+        self.opt = dict(OPT)  # per generator: generation may run on several threads
         self.vars = dp.vars
         off, stk = 0, {}
         for v in range(len(dp.vars)):
@@ -98,6 +103,8 @@ class _Gen:
         self.cache: set[int] = set()
         self.cached_vars: set[int] = set()
         self.pre: list[str] = []
+        self.pm: dict[int, int] | None = None  # paired block: var of block A -> var of block B
+        self.pair_ops = None                   # ... and block B's ops (per-lane immediates)
 
     # ---- operand access -----------------------------------------------------------------
     def w(self, v):
@@ -109,11 +116,46 @@ class _Gen:
     def local(self, v, locals_):
         return v in locals_
 
-    def base(self, v):
-        """Row expression of the variable's slot 0."""
+    def imm0(self, k, op) -> str:
+        """imm0 of op k as an expression (a paired block's vslice may differ per lane)."""
+        a = int(op["imm0"])
+        if self.pm is not None and self.pair_ops is not None:
+            bb = int(self.pair_ops[k]["imm0"])
+            if bb != a:
+                return f"(sB_ ? {bb} : {a})"
+        return str(a)
+
+    def _pair(self, v):
+        """The partner block's variable at v's position (paired blocks), or None."""
+        if self.pm is None:
+            return None
+        u = self.pm.get(v, v)
+        return None if u == v else u
+
+    def _base1(self, v):
         if self.cls(v) == STACKED:
             return f"({self.flat} + D * {self.stk[v]})"
         return str(int(self.vars[v]["row"]))
+
+    def base(self, v):
+        """Row expression of the variable's slot 0 (per lane in a paired block)."""
+        u = self._pair(v)
+        if u is None or self._base1(u) == self._base1(v):
+            return self._base1(v)
+        return f"(sB_ ? {self._base1(u)} : {self._base1(v)})"
+
+    def spr(self, v):
+        """Stack-pointer row expression of stacked variable v (per lane in a paired block)."""
+        r = int(self.vars[v]["sp"])
+        u = self._pair(v)
+        if u is None or int(self.vars[u]["sp"]) == r:
+            return str(r)
+        return f"(sB_ ? {int(self.vars[u]['sp'])} : {r})"
+
+    def vid(self, v):
+        """Variable id expression for fault reports."""
+        u = self._pair(v)
+        return str(v) if u is None else f"(sB_ ? {u} : {v})"
 
     def ptr(self, v):
         """Pointer expression to the variable's current top (read)."""
@@ -121,11 +163,18 @@ class _Gen:
             r = int(self.vars[v]["sp"])
             if self.in_seg:  # stack pointer cached in a register for the segment
                 return f"ln.row({self.base(v)} + (sp{r} > 0 ? sp{r} - 1 : 0) * {self.w(v)})"
-            return f"ln.top({self.base(v)}, {r}, {self.w(v)})"
+            return f"ln.top({self.base(v)}, {self.spr(v)}, {self.w(v)})"
         return f"ln.row({self.base(v)})"
 
     def disjoint(self, dv, act, sv, d_off, s_off, w):
         """Can a copy of w words from sv(+s_off) to dv(+d_off) use the no-alias helper?"""
+        if self.pm is not None:  # must hold for both blocks of a pair
+            pm, self.pm = self.pm, None
+            try:
+                return (self.disjoint(dv, act, sv, d_off, s_off, w) and
+                        self.disjoint(pm.get(dv, dv), act, pm.get(sv, sv), d_off, s_off, w))
+            finally:
+                self.pm = pm
         if dv == sv:
             return act == PUSH  # a push writes a fresh slot above the top it reads
         if self.cls(dv) == STACKED or self.cls(sv) == STACKED:
@@ -136,6 +185,13 @@ class _Gen:
 
     def same_rows(self, dv, act, sv, d_off, s_off):
         """Statically the same storage (an in-place chain link): the copy is a no-op."""
+        if self.pm is not None:  # must hold for both blocks of a pair
+            pm, self.pm = self.pm, None
+            try:
+                return (self.same_rows(dv, act, sv, d_off, s_off) and
+                        self.same_rows(pm.get(dv, dv), act, pm.get(sv, sv), d_off, s_off))
+            finally:
+                self.pm = pm
         if act == PUSH:
             return False
         if self.cls(dv) == STACKED or self.cls(sv) == STACKED:
@@ -145,9 +201,9 @@ class _Gen:
     def copy(self, w, dst_expr, src_expr, dv, act, sv, d_off=0, s_off=0):
         if self.same_rows(dv, act, sv, d_off, s_off):
             return "  /* in place */"
-        if OPT["staged"] and w >= 16:
+        if self.opt["staged"] and w >= 16:
             return f"  copy_staged<{w}>({dst_expr}, {src_expr}, sm);"
-        fn = "copy_nr" if OPT["noalias"] and self.disjoint(dv, act, sv, d_off, s_off, w) else "copy"
+        fn = "copy_nr" if self.opt["noalias"] and self.disjoint(dv, act, sv, d_off, s_off, w) else "copy"
         return f"  {fn}<{w}>({dst_expr}, {src_expr});"
 
     def scalar(self, v, locals_):
@@ -182,11 +238,11 @@ class _Gen:
         if act == POP:
             sp = int(self.vars[out]["sp"])
             if not self.in_seg:
-                return [f"{{ int& s_ = ln.sp_row({sp});",
-                        f"  if (s_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                return [f"{{ int& s_ = ln.sp_row({self.spr(out)});",
+                        f"  if (s_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {self.vid(out)}, 0}}; ok = false; goto {self.end}; }}",
                         "  --s_; }"]
             self.dirty.add(sp)
-            lines += [f"if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+            lines += [f"if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {self.vid(out)}, 0}}; ok = false; goto {self.end}; }}",
                       f"--sp{sp};"]
             return lines
         width = int(op["width"])
@@ -240,13 +296,13 @@ class _Gen:
             expr = (f"({P(0)})[clip(to_i64({S(1)}, {str(self.vars[ins[1]]['kind'] == F64).lower()}), "
                     f"{W(0)}) * S]")
         elif name == "vslice" and width == 1:
-            expr = f"({P(0)})[{int(op['imm0'])} * S]"
+            expr = f"({P(0)})[{self.imm0(k, op)} * S]"
         elif name == "vfill" and width == 1:
             expr = S(0)
         elif name == "rng_uniform":
             kf = str(self.vars[ins[0]]["kind"] == F64).lower()
             cf = str(self.vars[ins[1]]["kind"] == F64).lower()
-            expr = (f"ool_rng(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf}))" if OPT["ool"] else
+            expr = (f"ool_rng(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf}))" if self.opt["ool"] else
                     f"f64_bits(lsb::rng_uniform(to_i64({S(0)}, {kf}), to_i64({S(1)}, {cf})))")
         elif name == "dot":
             expr = f"f64_bits(dot<{W(0)}>({P(0)}, {P(1)}))"
@@ -269,8 +325,11 @@ class _Gen:
         elif name == "id":
             lines.append(self.copy(width, "d_", P(0), out, act, ins[0]))
         elif name == "vslice":
-            lo = int(op["imm0"])
-            lines.append(self.copy(width, "d_", f"{P(0)} + {lo} * S", out, act, ins[0], 0, lo))
+            lo = self.imm0(k, op)
+            if lo.isdigit():
+                lines.append(self.copy(width, "d_", f"{P(0)} + {lo} * S", out, act, ins[0], 0, int(lo)))
+            else:  # per-lane window offset (paired blocks): a plain copy
+                lines.append(f"  copy<{width}>(d_, {P(0)} + {lo} * S);")
         elif name == "vcat":
             wa = W(0)
             lines.append(self.copy(wa, "d_", P(0), out, act, ins[0]))
@@ -298,7 +357,7 @@ class _Gen:
                         "min": "i_min(xs_[i * S], ys_[i * S], true)",
                         "max": "i_min(xs_[i * S], ys_[i * S], false)"}[name]
             code = {"add": 0, "sub": 1, "mul": 2, "div": 3}.get(name)
-            if OPT["ool"] and fk and code is not None:
+            if self.opt["ool"] and fk and code is not None:
                 lines.append(f"  binop_f64_n(d_, {xs}, {ys}, {width}, {code});")
             else:
                 lines.append(f"  {{ const uint64_t* xs_ = {xs}; const uint64_t* ys_ = {ys};")
@@ -323,21 +382,22 @@ class _Gen:
         if self.cls(out) != STACKED:
             return [f"{{ uint64_t* d_ = ln.row({self.base(out)});"], []
         sp = int(self.vars[out]["sp"])
+        vo = self.vid(out)
         if self.in_seg:  # stack pointer cached in the segment's register sp<row>
             if act == PUSH:
                 self.dirty.add(sp)
-                return ([f"{{ if (sp{sp} >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+                return ([f"{{ if (sp{sp} >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {vo}, 0}}; ok = false; goto {self.end}; }}",
                          f"  uint64_t* d_ = ln.row({self.base(out)} + sp{sp} * {width});"],
                         [f"  ++sp{sp};"])
-            return ([f"{{ if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 1}}; ok = false; goto {self.end}; }}",
+            return ([f"{{ if (sp{sp} < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {vo}, 1}}; ok = false; goto {self.end}; }}",
                      f"  uint64_t* d_ = ln.row({self.base(out)} + (sp{sp} - 1) * {width});"], [])
         if act == PUSH:
-            return ([f"{{ int& sp_ = ln.sp_row({sp});",
-                     f"  if (sp_ >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {out}, 0}}; ok = false; goto {self.end}; }}",
+            return ([f"{{ int& sp_ = ln.sp_row({self.spr(out)});",
+                     f"  if (sp_ >= D) {{ f = StepFault{{{pos}, LS_RUN_OVERFLOW, {vo}, 0}}; ok = false; goto {self.end}; }}",
                      f"  uint64_t* d_ = ln.row({self.base(out)} + sp_ * {width});"],
                     ["  ++sp_;"])
-        return ([f"{{ const int sp_ = ln.sp_row({sp});",
-                 f"  if (sp_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {out}, 1}}; ok = false; goto {self.end}; }}",
+        return ([f"{{ const int sp_ = ln.sp_row({self.spr(out)});",
+                 f"  if (sp_ < 1) {{ f = StepFault{{{pos}, LS_RUN_UNDERFLOW, {vo}, 1}}; ok = false; goto {self.end}; }}",
                  f"  uint64_t* d_ = ln.row({self.base(out)} + (sp_ - 1) * {width});"], [])
 
     def leapfrog_fn(self, t: int) -> str:
@@ -630,10 +690,92 @@ class _Gen:
             out_lines[ks[m]] = (max(h, ks[m - window] + 1), line)
         return out_lines
 
-    def block(self, b):
+    def block_ops(self, b):
+        blk = self.dp.blocks[b]
+        return self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
+
+    def pair_map(self, a, b) -> dict[int, int] | None:
+        """Variable correspondence when blocks a and b are the same code on different storage
+        (op by op: opcode, action, width, immediates, operand classes and widths; terminator
+        kind), e.g. the two direction variants of NUTS-lite's tree calls and landing pads.
+        Such a pair runs in one warp step, each lane on its own block's variables."""
+        ba, bb = self.dp.blocks[a], self.dp.blocks[b]
+        if int(ba["term"]) != int(bb["term"]) or int(ba["op_count"]) != int(bb["op_count"]):
+            return None
+        if int(ba["grads"]) or int(bb["grads"]):
+            return None
+        pm: dict[int, int] = {}
+
+        def match(u, v):
+            if pm.get(u, v) != v or self.cls(u) != self.cls(v) or self.w(u) != self.w(v):
+                return False
+            if self.dp.types[self.dp.var_names[u]] != self.dp.types[self.dp.var_names[v]]:
+                return False
+            pm[u] = v
+            return True
+
+        for x, y in zip(self.block_ops(a), self.block_ops(b)):
+            if self.is_coop(x) or self.is_coop(y):
+                return None
+            # a vslice may take its window at a different offset in each block (per-lane offset)
+            fields = ("opcode", "action", "nin", "kind", "width", "imm2", "bits")
+            if OP.get(int(x["opcode"])) != "vslice":
+                fields += ("imm0", "imm1")
+            for f in fields:
+                if int(x[f]) != int(y[f]):
+                    return None
+            if not match(int(x["out"]), int(y["out"])):
+                return None
+            for j in range(int(x["nin"])):
+                if not match(int(x["in"][j]), int(y["in"][j])):
+                    return None
+        if int(ba["term"]) == 1 and not match(int(ba["cond"]), int(bb["cond"])):
+            return None
+        if len(set(pm.values())) != len(pm):  # a bijection of variables
+            return None
+        return pm
+
+    def find_pairs(self) -> dict[int, int]:
+        """Disjoint block pairs that can share a warp step (block -> partner)."""
+        n = len(self.dp.blocks)
+        out: dict[int, int] = {}
+        if not self.opt["pairs"]:
+            return out
+        sig = {}
+        for b in range(n):
+            ops = self.block_ops(b)
+            key = (int(self.dp.blocks[b]["term"]), tuple((int(o["opcode"]), int(o["width"])) for o in ops))
+            sig.setdefault(key, []).append(b)
+        for group in sig.values():
+            for i, a in enumerate(group):
+                if a in out or not len(self.block_ops(a)):
+                    continue
+                for b2 in group[i + 1:]:
+                    if b2 not in out and self.pair_map(a, b2) is not None:
+                        out[a], out[b2] = b2, a
+                        break
+        return out
+
+    def block(self, b, partner: int | None = None):
         blk = self.dp.blocks[b]
         ops = self.dp.ops[int(blk["op_begin"]):int(blk["op_begin"]) + int(blk["op_count"])]
-        if OPT["interp_min"] and len(ops) > OPT["interp_min"]:
+        self.pm = self.pair_map(b, partner) if partner is not None else None
+        if partner is not None and self.pm is None:
+            raise AssertionError("not a block pair")
+        if self.pm is not None:
+            saved_opt = {k: self.opt[k] for k in ("hoist", "ewdot", "fanout")}
+            self.opt.update(hoist=0, ewdot=0, fanout=0)  # their static row reasoning is per block
+            self.pair_ops = self.block_ops(partner)
+            try:
+                return self._block(b, blk, ops, partner)
+            finally:
+                self.opt.update(saved_opt)
+                self.pm = None
+                self.pair_ops = None
+        return self._block(b, blk, ops, None)
+
+    def _block(self, b, blk, ops, partner):
+        if self.opt["interp_min"] and len(ops) > self.opt["interp_min"] and partner is None:
             return (f"__device__ {_block_qual()} bool gb_{b}(const VMArgs& a, const Lane ln, bool active, "
                     f"long long chain, StepFault& f, double* sm, int& pc_, int& psp_) {{\n"
                     f"  int& msp_ = ln.sp_row(a.n_sp_rows - 1);  // the interpreter keeps pc state in memory\n"
@@ -657,6 +799,8 @@ class _Gen:
                 f"long long chain, StepFault& f, double* sm, int& pc_, int& psp_) {{",
                 "  const int D = a.depth; (void)D; (void)sm; (void)chain;",
                 "  bool ok = active;"]
+        if partner is not None:
+            body.append(f"  const bool sB_ = pc_ == {partner};  // this lane runs block {partner} (paired with {b})")
         if locals_:
             body.append("  uint64_t " + ", ".join(f"s{v} = 0" for v in sorted(locals_)) + ";")
         decl_at = len(body)
@@ -678,20 +822,23 @@ class _Gen:
                 j += 1
             # stack pointers this segment touches: loaded once (in parallel), written back if moved
             rows = set()
+            row_expr: dict[int, str] = {}
             for op in ops[i:j]:
                 for v in [int(op["out"]), *[int(x) for x in op["in"][:int(op["nin"])]]]:
                     if self.cls(v) == STACKED:
                         rows.add(int(self.vars[v]["sp"]))
+                        row_expr[int(self.vars[v]["sp"])] = self.spr(v)
             all_sp |= rows
-            self.in_seg, self.dirty = OPT["spcache"], set()
-            if not OPT["spcache"]:
+            self.in_seg, self.dirty = self.opt["spcache"], set()
+            if not self.opt["spcache"]:
                 rows = set()
             body.append(f"  const bool ran{seg} = ok;")
             body.append("  if (ok) {")
-            body += [f"    sp{r} = ln.sp_row({r});" for r in sorted(rows)]
-            hoisted = self.hoistable_loads(ops, i, j, locals_) if OPT["hoist"] else {}
-            fused = self.ew_dot_fusions(ops, i, j, locals_, blk) if OPT["ewdot"] else {}
-            if OPT["fanout"]:
+            body += [f"    sp{r} = ln.sp_row({row_expr[r]});" for r in sorted(rows)]
+            self.row_expr = row_expr
+            hoisted = self.hoistable_loads(ops, i, j, locals_) if self.opt["hoist"] else {}
+            fused = self.ew_dot_fusions(ops, i, j, locals_, blk) if self.opt["ewdot"] else {}
+            if self.opt["fanout"]:
                 for k, lines in self.copy_fanouts(ops, i, j, set(fused) | set(hoisted)).items():
                     fused.setdefault(k, lines)
             at: dict[int, list[str]] = {}
@@ -708,11 +855,18 @@ class _Gen:
             body.append("  }")
             body.append(f"  {self.end}:;")
             if self.dirty:
-                body.append(f"  if (ran{seg}) {{ " + " ".join(f"ln.sp_row({r}) = sp{r};" for r in sorted(self.dirty)) + " }")
+                body.append(f"  if (ran{seg}) {{ " + " ".join(f"ln.sp_row({row_expr[r]}) = sp{r};"
+                                                          for r in sorted(self.dirty)) + " }")
             self.in_seg = False
             seg += 1
         # terminator
-        term, ta, tb = int(blk["term"]), int(blk["a"]), int(blk["b"])
+        term, ta, tb = int(blk["term"]), str(int(blk["a"])), str(int(blk["b"]))
+        if partner is not None:
+            pb = self.dp.blocks[partner]
+            if int(pb["a"]) != int(blk["a"]):
+                ta = f"(sB_ ? {int(pb['a'])} : {ta})"
+            if int(pb["b"]) != int(blk["b"]):
+                tb = f"(sB_ ? {int(pb['b'])} : {tb})"
         body.append("  if (!ok) return false;")
         if self.cached_vars:
             body.insert(decl_at, "  uint64_t " + ", ".join(f"r{v} = 0" for v in sorted(self.cached_vars)) + ";")
@@ -732,8 +886,8 @@ class _Gen:
         n = len(self.dp.blocks)
         out = ["// generated by paper_1910_11141_b200/codegen.py — do not edit",
                f"// options: {sorted(OPT.items())}", "#pragma once",
-               f"#define LSB_GEN_STAGED {int(OPT['staged'])}",
-               f"#define LSB_GEN_OOL {int(OPT['ool'])}",
+               f"#define LSB_GEN_STAGED {int(self.opt['staged'])}",
+               f"#define LSB_GEN_OOL {int(self.opt['ool'])}",
                '#include "lsb_gen_rt.cuh"', "namespace lsbgen {",
                "// The current pc and pc-stack pointer live in registers (the engine writes them",
                "// back when a launch ends); memory keeps only the return addresses below the top.",
@@ -754,16 +908,28 @@ class _Gen:
                "      return pc == a.halt;",
                "  }",
                "}"]
+        pairs = self.find_pairs()
         for b in range(n):
-            out.append(self.block(b))
+            if b in pairs and pairs[b] < b:
+                continue  # generated with its partner
+            out.append(self.block(b, pairs.get(b)))
         out.append("__device__ __forceinline__ bool gen_exec_block(const VMArgs& a, const Lane& ln, int b, bool active,")
         out.append("                                               long long chain, StepFault& f, double* sm,")
         out.append("                                               int& pc_, int& psp_) {")
         out.append("  switch (b) {")
         for b in range(n):
-            out.append(f"    case {b}: return gb_{b}(a, ln, active, chain, f, sm, pc_, psp_);")
+            fb = min(b, pairs[b]) if b in pairs else b
+            out.append(f"    case {b}: return gb_{fb}(a, ln, active, chain, f, sm, pc_, psp_);")
         out.append("  }")
         out.append("  return false;")
+        out.append("}")
+        out.append("// the block whose lanes share a warp step with block b (identical code), or -1")
+        out.append("__device__ __forceinline__ int gen_pair(int b) {")
+        out.append("  switch (b) {")
+        for b, pb in sorted(pairs.items()):
+            out.append(f"    case {b}: return {pb};")
+        out.append("  }")
+        out.append("  return -1;")
         out.append("}")
         out.append("}  // namespace lsbgen")
         return "\n".join(out) + "\n"
@@ -789,7 +955,7 @@ def library_for(dp: DeviceProgram, *, build: bool = True, verbose: bool = False)
     tmp = lib.with_suffix(".so.tmp")
     cmd = [_build._nvcc(), *_build.NVCC_FLAGS, "-diag-suppress", "177,550", "-I", str(_build.ROOT / "include"), "-I", str(_build.CSRC),
            f"-DLSB_GENERATED=\"{hdr}\"", f"-DLSB_BPF={OPT['bpf']}", f"-DLSB_EW_UNROLL={OPT['ewu']}",
-           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_BLOCK_PROFILE={OPT['bprof']}", f"-DLSB_LF_KC={OPT['lfkc']}",
+           f"-DLSB_SB_PROFILE={OPT['sbprof']}", f"-DLSB_BLOCK_PROFILE={OPT['bprof']}", f"-DLSB_WARPS_MAX={OPT['wmax']}", f"-DLSB_LF_KC={OPT['lfkc']}",
            f"-DLSB_SB_INLINE={OPT['sbinline']}", f"-DLSB_WG_INLINE={OPT['wginline']}", "-o", str(tmp), str(_build.CSRC / "engine.cu")]
     if verbose:
         print(" ".join(cmd))

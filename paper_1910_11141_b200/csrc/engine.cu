@@ -203,15 +203,20 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
 #endif
 }
 
-// up to 16 warps per CTA (one CTA per SM when a target is staged); 128 registers
-constexpr int kWarpCtaMax = 16;
+// up to LSB_WARPS_MAX warps per CTA (one CTA per SM): 16 -> 128 registers per thread (the
+// fp64 DMMA superblock keeps the momentum in registers); builds for the fp32 arm may trade
+// registers for more resident warps (24 -> 85 registers), since its superblock works in TMEM
+#ifndef LSB_WARPS_MAX
+#define LSB_WARPS_MAX 16
+#endif
+constexpr int kWarpCtaMax = LSB_WARPS_MAX;
+static_assert(kWarpCtaMax % 4 == 0 && kWarpCtaMax <= 32, "warpgroups of 4 warps, at most 8 per CTA");
 
-// One warp's 32-lane group: the step loop of the warp engine. With a.wg the 4 warps of a
-// warpgroup choose one block per step together (a named barrier per step) — the fp32 arm's
-// tensor-core superblock runs the warpgroup's 128 chains at once.
+// One warp's 32-lane group: the step loop of the warp engine. Warps step independently; in
+// the fp32 arm the warps of a warpgroup meet only at the tensor-core superblock
+// (wg_rendezvous), which then runs all their chains at once.
 __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int wq = wid & 3, wgi = wid >> 2;
   const int g = blockIdx.x * (blockDim.x >> 5) + wid;
   constexpr int L = 32;
   const Lane ln{a.ws + (size_t)g * a.group_rows * L, a.sp + (size_t)g * a.n_sp_rows * L,
@@ -237,11 +242,9 @@ __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem)
     pc_r = ln.pcs[(psp_r - 1) * L + lane];
   }
 #endif
-  int par = 0;           // warpgroup step-slot parity
-  bool faulted = false;  // warpgroup mode: stop the warpgroup at the next step
 
   for (;;) {
-    if (chain == -1 && !faulted) {
+    if (chain == -1) {
       const unsigned long long c = atomicAdd(a.next_chain, 1ull);
       if ((long long)c < a.z) {
         chain = (long long)c;
@@ -274,45 +277,30 @@ __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem)
       // keys carry the block index in their low 16 bits (host: schedule.block_keys)
       key = pc == a.halt ? 0xffffffffu : lane_key(a, pc, depth_now);
       best = __reduce_min_sync(kFull, key);
-      if (a.wg) {  // the warpgroup agrees on one block (and on stopping)
-        const bool stop = faulted || ((steps & 15) == 0 && *(volatile int*)a.abort_flag) ||
-                          (a.max_steps >= 0 && steps >= a.max_steps);
-        if (lane == 0) {
-          lsb_tcs.key[wgi][par][wq] = best;
-          lsb_tcs.stop[wgi][par][wq] = stop;
-        }
-        wg_bar(wgi);
-        unsigned m = 0xffffffffu;
-        int any_stop = 0;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          m = min(m, lsb_tcs.key[wgi][par][w]);
-          any_stop |= lsb_tcs.stop[wgi][par][w];
-        }
-        par ^= 1;
-        if (any_stop && m != 0xffffffffu) {
-          if (!faulted && a.max_steps >= 0 && steps >= a.max_steps && lane == 0) a.paused[0] = 1;
-          break;
-        }
-        best = m;
-      }
       b = best == 0xffffffffu ? a.halt : (int)(best & 0xffffu);
     }
     if (b == a.halt) {
       if (lane == 0) a.group_done[g] = 1;
       break;
     }
-    if (!a.wg) {
-      // another group's fault stops this one within 16 steps (one flag read per 16 steps)
-      if ((steps & 15) == 0 && *(volatile int*)a.abort_flag) break;
-      if (a.max_steps >= 0 && steps >= a.max_steps) {
-        if (lane == 0) a.paused[0] = 1;
-        break;
-      }
+    // another group's fault stops this one within 16 steps (one flag read per 16 steps)
+    if ((steps & 15) == 0 && *(volatile int*)a.abort_flag) break;
+    if (a.max_steps >= 0 && steps >= a.max_steps) {
+      if (lane == 0) a.paused[0] = 1;
+      break;
     }
-    const bool active = a.sched == LS_SCHED_MOST_POPULATED ? pc == b : (pc != a.halt && key == best);
+    // specialised builds run a block and its partner (identical code on other variables,
+    // codegen.find_pairs) in one step, each lane on its own block
+#ifdef LSB_GENERATED
+    const int pb = a.sched == LS_SCHED_LOCAL ? -1 : lsbgen::gen_pair(b);
+#else
+    const int pb = -1;
+#endif
+    const bool active = (a.sched == LS_SCHED_MOST_POPULATED ? pc == b : (pc != a.halt && key == best)) ||
+                        (pb >= 0 && pc == pb);
     const int count = __popc(__ballot_sync(kFull, active));
-    if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, b);
+    const int count_pb = pb >= 0 ? __popc(__ballot_sync(kFull, active && pc == pb)) : 0;
+    if (active && a.lane_trace != nullptr) lane_trace_put(a, chain, pc);
     StepFault f;
 #if LSB_BLOCK_PROFILE
     const long long t_start = clock64();
@@ -336,16 +324,14 @@ __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem)
         fr.key = (unsigned long long)chain;
         fr.kind = f.kind;
         fr.var = f.var;
-        fr.block = b;
+        fr.block = pc;  // the lane's own block (b or its partner)
         fr.detail = f.detail;
         fr.chain = chain;
         __threadfence();
         atomicExch(a.abort_flag, 1);
       }
       ++steps;
-      if (!a.wg) break;
-      faulted = true;  // tell the warpgroup at the next step
-      continue;
+      break;
     }
     const unsigned hmask = __ballot_sync(kFull, halted_now);
     if (hmask) {
@@ -357,10 +343,18 @@ __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem)
     }
     if (lane == 0) {
       const int grads = __ldg(&a.blocks[b].grads);
+      const int count_b = count - count_pb;
       atomicAdd((unsigned long long*)&bsteps[b], 1ull);
-      atomicAdd((unsigned long long*)&bactive[b], (unsigned long long)count);
-      useful += (unsigned long long)count * (unsigned long long)grads;
+      atomicAdd((unsigned long long*)&bactive[b], (unsigned long long)count_b);
+      useful += (unsigned long long)count_b * (unsigned long long)grads;
       launched += (unsigned long long)L * (unsigned long long)grads;
+      if (count_pb) {
+        const int grads_pb = __ldg(&a.blocks[pb].grads);
+        atomicAdd((unsigned long long*)&bsteps[pb], 1ull);
+        atomicAdd((unsigned long long*)&bactive[pb], (unsigned long long)count_pb);
+        useful += (unsigned long long)count_pb * (unsigned long long)grads_pb;
+        launched += (unsigned long long)L * (unsigned long long)grads_pb;
+      }
     }
     ++steps;
   }
@@ -388,8 +382,8 @@ __global__ void __launch_bounds__(32 * kWarpCtaMax, 1) vm_warp_kernel(const __gr
   }
   if (a.tc_img != nullptr) tc_cta_begin(a, reinterpret_cast<unsigned char*>(lf_smem));
   const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  // warpgroup mode: every warp of a warpgroup takes part in its steps (groups come in 4s)
-  if (g < a.n_groups && (a.wg || !a.group_done[g])) warp_group_run(a, lf_smem);
+  if (g < a.n_groups && !a.group_done[g]) warp_group_run(a, lf_smem);
+  if (a.wg) wg_leave();  // peers stop waiting for this warp at their superblocks
   if (a.tc_img != nullptr) tc_cta_end();
 }
 
@@ -849,10 +843,6 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     if (m->opts.flags & LS_MF_FP32) {
       // fp32 arm: the superblock target's precision matrix as a TF32 hi/lo image (UMMA K-major,
       // no swizzle) that each CTA bulk-copies into shared memory in place of the DMMA fragments
-      if (m->opts.sched == LS_SCHED_MOST_POPULATED) {
-        delete m;
-        return fail(LS_EINVAL, "the fp32 arm steps warpgroups together: use a keyed schedule");
-      }
       if (st < 0 || !one || p->targets[st].kind != LS_TARGET_GAUSSIAN || p->targets[st].dim > 128) {
         delete m;
         return fail(LS_EINVAL, "the fp32 arm needs fused leapfrogs of one gaussian target with d <= 128");
@@ -860,6 +850,9 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       m->fp32 = true;
       m->stage_target = -1;
       m->stage_doubles = 0;
+      // the tensor-core superblock needs no per-warp shared tiles; other DMMA contractions
+      // (e.g. the iteration's initial logpdf) then read their A operand from the workspace
+      m->lf_smem_per_warp = 0;
       const int d = p->targets[st].dim, K = (d + 7) / 8 * 8, N = (d + 15) / 16 * 16;
       std::vector<float> P32((size_t)K * N, 0.f);
       const std::vector<double>& hp = p->host_params[st];

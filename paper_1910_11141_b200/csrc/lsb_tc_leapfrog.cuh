@@ -3,8 +3,9 @@
 //
 // Same function as warp_leapfrog_rp (reference workloads.py:461-472: L leapfrog steps of
 // g = -(q P), p = (e/2) g + p, q = e p + q, each multiply and add rounded separately),
-// computed in float32 for the 128 chains of a warpgroup at once (the warp engine steps
-// the warpgroup's 4 warps together in fp32 mode, so all of them are in this block):
+// computed in float32 for the chains of a warpgroup at once: the warps of a warpgroup step
+// independently and meet here (wg_rendezvous: every warp of the warpgroup that has not
+// finished arrives at its next superblock step), then run one 128-row contraction:
 //
 //   TMEM (512 columns, one warpgroup at a time per CTA):
 //     [  0, 128)  D  = q . P (fp32 accumulators, N = d rounded up to 16)
@@ -31,14 +32,74 @@ struct TcShared {
   int pad;
   uint64_t mma_bar;
   uint64_t img_bar;
-  unsigned key[4][2][4];    // warpgroup step slots [warpgroup][parity][warp]
-  int stop[4][2][4];
+  // superblock rendezvous of each warpgroup's warps (wg_rendezvous / wg_leave)
+  struct {
+    int lock, arrived, gone, gen, mask, present;
+  } rv[8];  // up to 32 warps per CTA
 };
 __shared__ TcShared lsb_tcs;
 
 constexpr uint32_t kTcColD = 0, kTcColHi = 128, kTcColLo = 256, kTcColP = 384;
 
-__device__ __forceinline__ void wg_bar(int wgi) { asm volatile("bar.sync %0, 128;" ::"r"(1 + wgi) : "memory"); }
+// named barrier of the `nthreads` threads of warpgroup wgi that take part in a superblock
+__device__ __forceinline__ void wg_bar(int wgi, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + wgi), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ void rv_lock(int* l) {
+  while (atomicCAS(l, 0, 1) != 0) __nanosleep(32);
+  __threadfence_block();
+}
+__device__ __forceinline__ void rv_unlock(int* l) {
+  __threadfence_block();
+  atomicExch(l, 0);
+}
+
+// Called by lane 0 with the warpgroup's rendezvous lock held: if every warp still running
+// has arrived, release them together (present = their mask) and start a new generation.
+__device__ __forceinline__ void rv_try_release(int wgi) {
+  auto& r = lsb_tcs.rv[wgi];
+  if (r.arrived > 0 && r.arrived + r.gone == 4) {
+    r.present = r.mask;
+    r.arrived = 0;
+    r.mask = 0;
+    __threadfence_block();
+    atomicAdd(&r.gen, 1);
+  }
+}
+
+// Whole warp: wait until every unfinished warp of this warpgroup is at its superblock step;
+// returns the mask (bit = warp index within the warpgroup) of the warps taking part.
+__device__ inline unsigned wg_rendezvous() {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wq = wid & 3, wgi = wid >> 2;
+  unsigned present = 0;
+  if (lane == 0) {
+    auto& r = lsb_tcs.rv[wgi];
+    rv_lock(&r.lock);
+    const int gen = *(volatile int*)&r.gen;
+    r.arrived += 1;
+    r.mask |= 1 << wq;
+    rv_try_release(wgi);
+    rv_unlock(&r.lock);
+    while (*(volatile int*)&r.gen == gen) __nanosleep(64);
+    __threadfence_block();
+    present = (unsigned)*(volatile int*)&r.present;
+  }
+  return __shfl_sync(0xffffffffu, present, 0);
+}
+
+// Whole warp, once when it stops stepping: peers no longer wait for it.
+__device__ inline void wg_leave() {
+  const int wid = threadIdx.x >> 5, wgi = wid >> 2;
+  if ((threadIdx.x & 31) == 0) {
+    auto& r = lsb_tcs.rv[wgi];
+    rv_lock(&r.lock);
+    r.gone += 1;
+    rv_try_release(wgi);
+    rv_unlock(&r.lock);
+  }
+  __syncwarp();
+}
 
 // Kernel prologue, every thread of the CTA: TMEM, barriers, the B image (bulk copy).
 __device__ inline void tc_cta_begin(const VMArgs& a, unsigned char* dyn) {
@@ -50,10 +111,7 @@ __device__ inline void tc_cta_begin(const VMArgs& a, unsigned char* dyn) {
     lsbtc::fence_barrier_init();
   }
   if (threadIdx.x < 32) lsbtc::tmem_alloc(&lsb_tcs.tmem, 512);
-  for (int i = threadIdx.x; i < 4 * 2 * 4; i += blockDim.x) {
-    (&lsb_tcs.key[0][0][0])[i] = 0xffffffffu;
-    (&lsb_tcs.stop[0][0][0])[i] = 0;
-  }
+  if (threadIdx.x < 8) lsb_tcs.rv[threadIdx.x] = {0, 0, 0, 0, 0, 0};
   lsbtc::tc_fence_before();
   __syncthreads();
   lsbtc::tc_fence_after();
@@ -108,10 +166,14 @@ __device__ void wg_leapfrog_tf32(const VMArgs& a, const Lane& ln, const ROp& op,
     }
     lane_trace_put(a, chain, head + 2);
   }
+  // meet the warpgroup's other unfinished warps; the lowest present warp issues the MMAs
+  const unsigned present = wg_rendezvous();
+  const int nthr = 32 * __popc(present);
+  const int issuer = __ffs(present) - 1;
   // own the CTA's tensor memory for this call
-  if (wq == 0 && lane == 0)
+  if (wq == issuer && lane == 0)
     while (atomicCAS(&lsb_tcs.lock, 0, 1) != 0) __nanosleep(64);
-  wg_bar(wgi);
+  wg_bar(wgi, nthr);
   uint32_t phase = *(volatile uint32_t*)&lsb_tcs.phase;
   const uint32_t tbase = lsb_tcs.tmem;
   const uint32_t tb = tbase + ((uint32_t)(32 * wq) << 16);  // this warp's lane quarter
@@ -133,7 +195,7 @@ __device__ void wg_leapfrog_tf32(const VMArgs& a, const Lane& ln, const ROp& op,
   }
   lsbtc::tmem_st_wait();
   lsbtc::tc_fence_before();
-  wg_bar(wgi);
+  wg_bar(wgi, nthr);
   lsbtc::tc_fence_after();
   const uint32_t idesc = lsbtc::idesc_tf32(128, NP);
   const uint32_t bimg = lsbtc::smem_u32(lsb_dyn_u8 + a.tc_smem_off);
@@ -157,10 +219,10 @@ __device__ void wg_leapfrog_tf32(const VMArgs& a, const Lane& ln, const ROp& op,
       }
       lsbtc::tmem_st_wait();
       lsbtc::tc_fence_before();
-      wg_bar(wgi);
+      wg_bar(wgi, nthr);
       lsbtc::tc_fence_after();
     }
-    if (wq == 0 && lane == 0) {  // D = q . P on the tensor cores (3xTF32)
+    if (wq == issuer && lane == 0) {  // D = q . P on the tensor cores (3xTF32)
 #pragma unroll 1
       for (int ks = 0; ks < KT; ++ks) {
         const uint64_t bh = lsbtc::smem_desc_nosw(bimg + ks * 2 * a.tc_lbo, a.tc_lbo, a.tc_sbo);
@@ -204,7 +266,7 @@ __device__ void wg_leapfrog_tf32(const VMArgs& a, const Lane& ln, const ROp& op,
     }
     lsbtc::tmem_st_wait();
     lsbtc::tc_fence_before();
-    wg_bar(wgi);  // D is consumed before the next contraction overwrites it
+    wg_bar(wgi, nthr);  // D is consumed before the next contraction overwrites it
     lsbtc::tc_fence_after();
   }
   // write back q, p and _ret = vcat(q, p) (each thread its own chain: coalesced rows)
@@ -234,8 +296,8 @@ __device__ void wg_leapfrog_tf32(const VMArgs& a, const Lane& ln, const ROp& op,
   }
   if (part && want_lp) my_lp[0] = f64_bits(gauss_lp_from_quad(tg.norm, quad));
   lsbtc::tc_fence_before();
-  wg_bar(wgi);
-  if (wq == 0 && lane == 0) {
+  wg_bar(wgi, nthr);
+  if (wq == issuer && lane == 0) {
     lsb_tcs.phase = phase;
     __threadfence_block();
     atomicExch(&lsb_tcs.lock, 0);

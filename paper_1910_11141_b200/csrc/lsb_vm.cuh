@@ -119,7 +119,7 @@ struct VMArgs {
   int* abort_flag;
   int* paused;
   const unsigned* bkey;         // [n_blocks] schedule key of each block (block index in bits 0..15)
-  // warpgroup stepping: the 4 warps of a warpgroup select one block per step together
+  // fp32 arm: the warps of a warpgroup meet at tensor-core superblocks (lsb_tc_leapfrog.cuh)
   int wg;
   // fp32 arm (lsb_tc_leapfrog.cuh): leapfrog superblocks on tcgen05 (3xTF32), the target's
   // precision matrix as a K-major TF32 hi/lo image staged in shared memory at byte offset

@@ -35,6 +35,12 @@ TEST_NUTS = [
 # single-leaf programs (entry = leapfrog) whose fused superblock the per-step test checks
 # against the reference's leapfrog vectors (tests/golden/leapfrog.npz)
 LEAPFROG = [(2, 1), (2, 4), (100, 1), (100, 4)]
+# BASELINE configs 3 and 5 as bench.py measures them (their own bench-line objects)
+CONFIG3 = dict(n=1000, d=25, seed=0, step_size=0.05, leaf_steps=4, max_depth=10, iterations=5)
+CONFIG5 = dict(dim=1000, rho=9999 / 10999, step_size=0.02, leaf_steps=4, max_depth=15, iterations=2)
+# the headline target with dispersed starting points and a smaller step: trees of varying depth,
+# so lanes of a warp diverge (the case program-counter autobatching exists for)
+DISPERSED = dict(dim=100, rho=0.5, step_size=0.1, leaf_steps=4, max_depth=10, iterations=10)
 # logistic-regression cases (DMMA two-GEMM gradient): gradient-only programs and one NUTS run
 LR_GRAD = [(200, 5, 7), (1000, 25, 0)]
 LR_NUTS = dict(n=200, d=5, seed=7, step_size=0.1, leaf_steps=2, max_depth=5, iterations=3)
@@ -62,7 +68,7 @@ def specs():
     from .workloads import corpus
 
     out = []
-    for kw in [BENCH, *TEST_NUTS]:
+    for kw in [BENCH, DISPERSED, *TEST_NUTS]:
         kw = dict(kw)
         dim, rho = kw.pop("dim"), kw.pop("rho")
         _, _, cp = nuts(dim, rho, **kw)
@@ -76,6 +82,13 @@ def specs():
     kw = dict(LR_NUTS)
     _, t, cp = lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
     out.append(("lr_nuts", cp, [VType("f64", t.dim), I64]))
+    kw = dict(CONFIG3)
+    _, t, cp = lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    out.append(("config3", cp, [VType("f64", t.dim), I64]))
+    kw = dict(CONFIG5)
+    dim, rho = kw.pop("dim"), kw.pop("rho")
+    _, _, cp = nuts(dim, rho, **kw)
+    out.append(("config5", cp, [VType("f64", dim), I64]))
     for e in corpus():
         cp = compile_program(compile_source(e.source, e.entry))
         ins = e.make_inputs(np.random.default_rng(0), 2)

@@ -614,7 +614,7 @@ def test_fp32_nuts_control_traces_match_the_f64_oracle(codegen):
         z, d = 200, t.dim
         ins = [np.zeros((z, d)), np.arange(z, dtype=np.int64) * 7919 + 11]
         ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
-        for sched in ("min_pc", "priority"):
+        for sched in ("min_pc", "priority", "most_populated"):
             got, tr, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=codegen,
                                exact_logpdf=False, precision="fp32", schedule=sched,
                                lane_trace_cap=1 << 16, return_machine=True)

@@ -2,7 +2,7 @@
 
 Runs one warm launch and prints, per flat block, steps, mean active lanes, total
 SM cycles (sum over warps) and share, from the device's clock64 accounting.
-usage: python tools/block_profile.py [chains] [codegen 0/1] [schedule]  (builds a LSB_CG_BPROF=1 library)
+usage: python tools/block_profile.py [chains] [codegen 0/1] [schedule] [fp64|fp32]  (builds a LSB_CG_BPROF=1 library)
 """
 import os
 import sys
@@ -17,12 +17,13 @@ from paper_1910_11141_b200 import prebuilt  # noqa: E402
 z = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 cg = (sys.argv[2] != "0") if len(sys.argv) > 2 else True
 sched = sys.argv[3] if len(sys.argv) > 3 else "priority"
+prec = sys.argv[4] if len(sys.argv) > 4 else "fp64"
 kw = dict(prebuilt.BENCH)
 cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
 q0 = np.zeros((z, t.dim))
 key = np.arange(z, dtype=np.int64) * 7919 + 11
 m = L.init_machine(cp, [q0, key], depth=cfg.min_stack_depth, engine="warp", optimize=True,
-                   exact_logpdf=False, codegen=cg, schedule=sched)
+                   exact_logpdf=False, codegen=cg, schedule=sched, precision=prec)
 m._h.run(-1)
 m._h.reset()
 st = m._h.run(-1)

@@ -28,5 +28,5 @@ for _ in range(3):
     st = m._h.run(-1)
     ms.append(st.kernel_ms)
 best = min(ms)
-print(f"{label:24s} {prec} z={z}: {best:.2f} ms  {st.useful_grads / best / 1e3:.1f} M grads/s  "
+print(f"{label:24s} {prec} z={z}: {best:.2f} ms  steps/warp {st.steps}  {st.useful_grads / best / 1e3:.1f} M grads/s  "
       f"frac {st.useful_grads / best * 1e3 * 2e4 / 1e12 / 37.0:.3f}", flush=True)
