@@ -549,7 +549,7 @@ def main():
             "headline target, q0 ~ N(0, I) per chain, step 0.1: tree depths vary across chains")
         kw = dict(prebuilt.CONFIG5)
         c5, t5, cp5 = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
-        cfg_point("config5_gauss1000_cond1e4_depth15", c5, t5, cp5, 1 << 11,
+        cfg_point("config5_gauss1000_cond1e4_depth15", c5, t5, cp5, 1 << 14,
                   lambda zz: [np.zeros((zz, t5.dim)), chain_keys(0, zz)])
 
     # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kMaxLanes) vm_cta_kernel(const __grid_constant
 #define LSB_WARPS_MAX 16
 #endif
 constexpr int kWarpCtaMax = LSB_WARPS_MAX;
-static_assert(kWarpCtaMax % 4 == 0 && kWarpCtaMax <= 32, "warpgroups of 4 warps, at most 8 per CTA");
+static_assert(kWarpCtaMax <= 32, "at most 8 warpgroups per CTA");
 
 // One warp's 32-lane group: the step loop of the warp engine. Warps step independently; in
 // the fp32 arm the warps of a warpgroup meet only at the tensor-core superblock
@@ -851,8 +851,7 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       m->stage_target = -1;
       m->stage_doubles = 0;
       // the tensor-core superblock needs no per-warp shared tiles; other DMMA contractions
-      // (e.g. the iteration's initial logpdf) then read their A operand from the workspace
-      m->lf_smem_per_warp = 0;
+      // (e.g. the iteration's initial logpdf) keep theirs when they fit beside the image
       const int d = p->targets[st].dim, K = (d + 7) / 8 * 8, N = (d + 15) / 16 * 16;
       std::vector<float> P32((size_t)K * N, 0.f);
       const std::vector<double>& hp = p->host_params[st];
@@ -869,10 +868,12 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
         return rc2;
       }
       CK(cudaMemcpy(m->tc_img, img.data(), img.size(), cudaMemcpyHostToDevice));
-      int wpc = kWarpCtaMax;
+      // one CTA per SM (it owns the SM's tensor memory), enough warps to cover the groups
+      int wpc = (int)std::min<long long>(kWarpCtaMax, std::max<long long>(4, (want + sms - 1) / sms));
       auto off_of = [&](int w) { return ((size_t)w * m->lf_smem_per_warp * sizeof(double) + 1023) / 1024 * 1024; };
-      while (wpc >= 4 && off_of(wpc) + img.size() > (size_t)smem_optin) wpc -= 4;
-      if (wpc < 4) {
+      if (off_of(wpc) + img.size() > (size_t)smem_optin) m->lf_smem_per_warp = 0;  // tiles do not fit
+      while (wpc >= 1 && off_of(wpc) + img.size() > (size_t)smem_optin) --wpc;
+      if (wpc < 1) {
         cudaFree(m->tc_img);
         delete m;
         return fail(LS_EINVAL, "the fp32 arm's shared-memory image does not fit");
@@ -894,10 +895,7 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     groups = m->opts.ctas > 0 ? 4 * m->opts.ctas
                               : (int)std::min<long long>(want, (long long)sms * m->warps_per_cta * per_sm);
     if (groups > want) groups = (int)want;
-    if (m->fp32) {  // whole CTAs of warpgroups (spare groups just find the chain queue empty)
-      const int wpc = m->warps_per_cta;
-      groups = m->opts.ctas > 0 ? wpc * m->opts.ctas : (groups + wpc - 1) / wpc * wpc;
-    }
+    if (m->fp32 && m->opts.ctas > 0) groups = m->warps_per_cta * m->opts.ctas;
   } else {
     int lanes = m->opts.lanes_per_cta > 0 ? m->opts.lanes_per_cta : (int)std::min<long long>(z, kMaxLanes);
     if (m->opts.lanes_per_cta <= 0 && z > kMaxLanes) {

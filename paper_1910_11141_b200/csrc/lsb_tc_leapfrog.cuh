@@ -111,7 +111,10 @@ __device__ inline void tc_cta_begin(const VMArgs& a, unsigned char* dyn) {
     lsbtc::fence_barrier_init();
   }
   if (threadIdx.x < 32) lsbtc::tmem_alloc(&lsb_tcs.tmem, 512);
-  if (threadIdx.x < 8) lsb_tcs.rv[threadIdx.x] = {0, 0, 0, 0, 0, 0};
+  if (threadIdx.x < 8) {  // warps a short last warpgroup lacks never arrive: count them as gone
+    const int nw = (int)(blockDim.x >> 5) - 4 * (int)threadIdx.x;
+    lsb_tcs.rv[threadIdx.x] = {0, 0, nw >= 4 ? 0 : (nw > 0 ? 4 - nw : 4), 0, 0, 0};
+  }
   lsbtc::tc_fence_before();
   __syncthreads();
   lsbtc::tc_fence_after();

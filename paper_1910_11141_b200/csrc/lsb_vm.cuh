@@ -462,6 +462,10 @@ __device__ __forceinline__ int mtile_lane(unsigned mask, int n, int mt, int g) {
   return idx < n ? (int)__fns(mask, 0, idx + 1) : -1;
 }
 
+// n-tiles (of 8 columns) up to which a target counts as narrow: the register-momentum
+// superblock and single-m-tile contractions; wider targets take warp_gauss_wide
+constexpr int kLfRegMaxTiles = 16;
+
 // The CTA's shared-memory copy of target `t`'s B fragments, or nullptr (warp engine).
 __device__ __forceinline__ const double* staged_B(const VMArgs& a, int t) {
   extern __shared__ double lsb_dyn_smem[];
@@ -509,6 +513,82 @@ template <bool SB, bool SX>
 __device__ inline void warp_gauss_impl(const DevTarget& tg, const double* Bf, bool part, const uint64_t* xp,
                                        uint64_t* dst, bool want_logpdf, double* Xs);
 
+// Wide gaussian targets (d > 128, e.g. BASELINE config 5 at d = 1000): the precision
+// matrix (8 MB at d = 1000) does not fit on chip, so every B fragment read from L2 feeds
+// all of the warp's m-tiles (up to 4 x 8 chains) and every A fragment 4 n-tiles: 8 DMMAs
+// per 6 fragment loads instead of 1 per 2. Accumulation order per output element and the
+// logpdf's fma order are warp_gauss_impl's, so results are bit-identical.
+__device__ __noinline__ void warp_gauss_wide(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+                                             bool want_logpdf) {
+  constexpr int NTC = 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2;
+  const unsigned mask = __ballot_sync(kFull, part);
+  const int n = __popc(mask);
+  if (n == 0) return;
+  const int MT = (n + 7) / 8;
+  const int d = tg.dim, KS = tg.KS1, NT = tg.NT1;
+  const uint64_t* xg[4];
+  uint64_t* dg[4];
+  bool okr[4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int src = mt < MT ? mtile_lane(mask, n, mt, g) : -1;
+    okr[mt] = src >= 0;
+    xg[mt] = (const uint64_t*)__shfl_sync(kFull, (unsigned long long)xp, src < 0 ? 0 : src);
+    dg[mt] = (uint64_t*)__shfl_sync(kFull, (unsigned long long)dst, src < 0 ? 0 : src);
+  }
+  double quad[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int nt0 = 0; nt0 < NT; nt0 += NTC) {
+    const int ntc = min(NTC, NT - nt0);
+    double acc[4][NTC][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) acc[mt][j][0] = acc[mt][j][1] = 0.0;
+    const double* bp = tg.B1 + (size_t)nt0 * 32 + lane;
+    const size_t kstride = (size_t)NT * 32;
+#pragma unroll 1
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + (lane & 3);
+      double av[4], bv[NTC];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = (okr[mt] && k < d) ? as_f64(xg[mt][(size_t)k * 32]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NTC; ++j) bv[j] = j < ntc ? lsb::ldg_keep(bp + j * 32) : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+        if (mt < MT) {  // warp-uniform
+#pragma unroll
+          for (int j = 0; j < NTC; ++j) lsb::dmma(acc[mt][j], av[mt], bv[j]);
+        }
+      bp += kstride;
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      if (!okr[mt]) continue;
+#pragma unroll
+      for (int j = 0; j < NTC; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * (nt0 + j) + 2 * (lane & 3) + e;
+          if (j < ntc && col < d) {
+            if (want_logpdf) quad[mt] = fma(as_f64(xg[mt][(size_t)col * 32]), acc[mt][j][e], quad[mt]);
+            else dg[mt][(size_t)col * 32] = f64_bits(-acc[mt][j][e]);
+          }
+        }
+    }
+  }
+  if (want_logpdf) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      double q = quad[mt];
+      q += __shfl_xor_sync(kFull, q, 1);
+      q += __shfl_xor_sync(kFull, q, 2);
+      if (okr[mt] && (lane & 3) == 0) dg[mt][0] = f64_bits(gauss_lp_from_quad(tg.norm, q));
+    }
+  }
+}
+
 // grad, or fast logpdf, of a gaussian target for every participating lane of the
 // warp (lane-minor storage, stride 32). xp/dst: this lane's input and output.
 // Bs: the staged B fragments (staged_B) or nullptr. sm/sm_doubles: the warp's
@@ -524,6 +604,10 @@ __device__ inline
 #endif
 void warp_gauss(const DevTarget& tg, const double* Bs, bool part, const uint64_t* xp,
                                   uint64_t* dst, bool want_logpdf, double* sm, int sm_doubles) {
+  if (tg.NT1 > kLfRegMaxTiles && Bs == nullptr) {
+    warp_gauss_wide(tg, part, xp, dst, want_logpdf);
+    return;
+  }
   const bool sx = sm != nullptr && 8 * lf_stride_q(tg.dim) <= sm_doubles;
   if (Bs) {
     if (sx) warp_gauss_impl<true, true>(tg, Bs, part, xp, dst, want_logpdf, sm);
@@ -714,8 +798,7 @@ __device__ __forceinline__ bool warp_coop(const VMArgs& a, const ROp& op) {
 // loads (8 rows x 4 cols, 64-bit) and C-fragment epilogues (8 rows x 2 cols,
 // 128-bit) are bank-conflict free.
 __host__ __device__ __forceinline__ int lf_stride_p(int d) { int s = (d + 7) / 8 * 8; return s + ((8 - s % 16) + 16) % 16; }
-// d <= 128 uses the register-momentum superblock (only q staged in shared memory)
-constexpr int kLfRegMaxTiles = 16;
+// d <= 128 uses the register-momentum superblock (only q staged in shared memory): kLfRegMaxTiles
 __host__ __device__ __forceinline__ int lf_smem_doubles(int d) {
   return (d + 7) / 8 <= kLfRegMaxTiles ? 8 * lf_stride_q(d) : 8 * (lf_stride_q(d) + lf_stride_p(d)) + 8;
 }
