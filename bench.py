@@ -365,7 +365,7 @@ def main():
         from paper_1910_11141_b200 import codegen
 
         lib = codegen.library_for(dp)  # prebuilt by __graft_entry__.build() for the default config
-    prog = _native.Program(dp, lib)
+    prog = _native.Program(dp, lib, device=local)  # this rank's GPU (LOCAL_RANK)
     mach = _native.MachineHandle(prog, z, cfg.min_stack_depth, sched=args.schedule,
                                  lanes_per_cta=0 if warp else args.lanes, ctas=args.groups,
                                  exact_logpdf=args.exact_logpdf, warp_groups=warp)
@@ -441,7 +441,7 @@ def main():
             if i == 2:
                 t0 = time.perf_counter()
                 g_e2e = 0
-            out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, engine=args.engine,
+            out, tr = L.run(cp, [q0, key], depth=cfg.min_stack_depth, engine=args.engine, device=local,
                             lanes_per_group=None if warp else args.lanes, groups=args.groups,
                             schedule=args.schedule, exact_logpdf=args.exact_logpdf,
                             codegen=warp and not args.no_codegen)
@@ -525,7 +525,7 @@ def main():
 
         def cfg_point(label, cfgx, tx, cpx, zz, inputs_fn):
             dtx = L.device_target(tx.name)
-            m2 = L.init_machine(cpx, inputs_fn(zz), depth=cfgx.min_stack_depth, engine="warp", optimize=True,
+            m2 = L.init_machine(cpx, inputs_fn(zz), depth=cfgx.min_stack_depth, engine="warp", optimize=True, device=local,
                                 exact_logpdf=False, codegen="cached", schedule=args.schedule)
             m2._h.run(-1)
             m2._h.reset()

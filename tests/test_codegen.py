@@ -1,0 +1,63 @@
+"""Program-specialised block code (codegen.py) on CPU: what gets generated, not run.
+
+* blocks with identical code on different variables (the two direction variants of
+  NUTS-lite's tree calls and landing pads) are paired into one warp step, each lane
+  on its own block's storage;
+* generation is deterministic and thread-safe (the prebuilt libraries are looked up
+  by the hash of the generated text, and build_all generates on several threads).
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from paper_1910_11141_b200 import codegen, prebuilt
+from paper_1910_11141_b200.lowering import lower
+from paper_1910_11141_b200.pc_vm import infer_types
+from paper_1910_11141_b200.runtime import I64, VType
+
+
+def _bench_dp():
+    kw = dict(prebuilt.BENCH)
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+    dp = lower(cp, infer_types(cp.flat, [VType("f64", t.dim), I64]), optimize=True, superblocks=True)
+    return cp, dp
+
+
+def test_direction_variants_are_paired():
+    cp, dp = _bench_dp()
+    pairs = codegen._Gen(dp).find_pairs()
+    named = {cp.labels[a]: cp.labels[b] for a, b in pairs.items() if a < b}
+    # the tree call sites (qp, pp) / (qm, pm), their landing copies and build_tree's pads
+    assert named["nuts_main.b11"] == "nuts_main.b12"
+    assert named["nuts_main.b14"] == "nuts_main.b15"
+    assert named["build_tree.b10"] == "build_tree.b11"
+    assert all(pairs[b] == a for a, b in pairs.items())  # symmetric, disjoint
+    src = codegen.generate(dp)
+    assert "const bool sB_ = pc_ == 12;" in src and "case 12: return gb_11(" in src
+    assert "__device__ __forceinline__ int gen_pair(int b)" in src
+    # the superblock and contraction blocks are never paired
+    for b in pairs:
+        assert int(dp.blocks[b]["grads"]) == 0
+
+
+def test_pair_map_rejects_different_code():
+    cp, dp = _bench_dp()
+    g = codegen._Gen(dp)
+    leaf = cp.labels.index("build_tree.b3")
+    merge = cp.labels.index("build_tree.b12")
+    assert g.pair_map(leaf, merge) is None
+    a, b = cp.labels.index("nuts_main.b11"), cp.labels.index("nuts_main.b12")
+    pm = g.pair_map(a, b)
+    assert pm is not None and len(set(pm.values())) == len(pm)
+
+
+def test_generation_is_deterministic_across_threads():
+    specs = prebuilt.specs()
+    dps = [lower(cp, infer_types(cp.flat, ts), optimize=True, superblocks=True) for _, cp, ts in specs]
+    serial = [codegen.generate(dp) for dp in dps]
+    with ThreadPoolExecutor(8) as ex:
+        threaded = list(ex.map(codegen.generate, dps))
+    assert serial == threaded
+    assert len({hash(s) for s in serial}) == len(set(serial))
+    assert np.all([("gb_0(" in s) for s in serial])
