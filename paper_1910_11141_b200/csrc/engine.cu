@@ -851,7 +851,9 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       m->stage_target = -1;
       m->stage_doubles = 0;
       // the tensor-core superblock needs no per-warp shared tiles; other DMMA contractions
-      // (e.g. the iteration's initial logpdf) keep theirs when they fit beside the image
+      // (the iteration's initial logpdf) read their A operand from the workspace (measured
+      // faster than staging it: the freed shared memory goes to L1)
+      m->lf_smem_per_warp = 0;
       const int d = p->targets[st].dim, K = (d + 7) / 8 * 8, N = (d + 15) / 16 * 16;
       std::vector<float> P32((size_t)K * N, 0.f);
       const std::vector<double>& hp = p->host_params[st];
@@ -871,7 +873,6 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       // one CTA per SM (it owns the SM's tensor memory), enough warps to cover the groups
       int wpc = (int)std::min<long long>(kWarpCtaMax, std::max<long long>(4, (want + sms - 1) / sms));
       auto off_of = [&](int w) { return ((size_t)w * m->lf_smem_per_warp * sizeof(double) + 1023) / 1024 * 1024; };
-      if (off_of(wpc) + img.size() > (size_t)smem_optin) m->lf_smem_per_warp = 0;  // tiles do not fit
       while (wpc >= 1 && off_of(wpc) + img.size() > (size_t)smem_optin) --wpc;
       if (wpc < 1) {
         cudaFree(m->tc_img);

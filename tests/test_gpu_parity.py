@@ -643,3 +643,25 @@ def test_fp32_refill_and_faults():
     assert (np.abs(got[pick] - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < 1e-4
     with pytest.raises(StackOverflow):
         L.run(cp, ins, depth=3, engine="warp", codegen="cached", exact_logpdf=False, precision="fp32")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_dispersed_workload_lanes_exact(precision):
+    """The bench's random-start workload (prebuilt.DISPERSED: q0 ~ N(0, I), step 0.1) through
+    its specialised library: every lane's pc trace equals the float64 oracle's; chains within
+    1e-9 (fp64) / 1e-4 (fp32). (The equicorrelated gaussian's U-turn time barely depends on
+    the state, so every chain builds trees of the same size here too.)"""
+    from paper_1910_11141_b200 import prebuilt
+    from paper_1910_11141_b200.distributed import chain_keys
+
+    kw = dict(prebuilt.DISPERSED)
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **dict(kw, iterations=kw["iterations"]))
+    z = 160
+    ins = [np.random.default_rng(1).standard_normal((z, t.dim)), chain_keys(0, z)]
+    ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+    got, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen="cached", exact_logpdf=False,
+                      schedule="priority", precision=precision, lane_trace_cap=1 << 16, return_machine=True)
+    for lane, seq in enumerate(m.lane_traces()):
+        assert np.array_equal(seq, ref.lane_blocks[lane]), lane
+    tol = CHAIN_RTOL if precision == "fp64" else 1e-4
+    assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < tol
