@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--chains", type=int, default=1 << 16, help="chains per GPU")
+    ap.add_argument("--config4-chains", type=int, default=1 << 12, help="config-4 line: chains")
+    ap.add_argument("--config5-chains", type=int, default=1 << 16, help="config-5 line: chains")
     ap.add_argument("--dim", type=int, default=100)
     ap.add_argument("--iterations", type=int, default=10)
     ap.add_argument("--depth", type=int, default=10)
@@ -69,7 +71,7 @@ def parse():
     ap.add_argument("--cpu-chains", type=int, default=256)
     ap.add_argument("--no-sweep", action="store_true", help="skip the 2^10..2^20 chain sweep")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 (tcgen05) arm")
-    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 3 and 5")
+    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 3, 4 and 5")
     ap.add_argument("--cpu-iterations", type=int, default=10)
     return ap.parse_args()
 
@@ -517,7 +519,7 @@ def main():
                 sweep[precision].append({"chains": zz, "value": v, "ms": ms,
                                          "frac": v * flops_per_grad / 1e12 / peak})
 
-    # BASELINE configs 3 and 5 (one warm + one timed launch each, fp64, same engine/schedule)
+    # BASELINE configs 3, 4 and 5 (one warm + one timed launch each, fp64, same engine/schedule)
     configs = None
     if rank == 0 and world == 1 and warp and not args.no_configs:
         configs = {}
@@ -550,9 +552,17 @@ def main():
             "headline target from random starts q0 ~ N(0, I), step 0.1; the equicorrelated gaussian's "
             "U-turn time barely depends on the state, so trees keep one size per iteration (config 3 "
             "is the workload whose chains diverge: see its grad_utilization)")
+        kw = dict(prebuilt.CONFIG4)
+        c4, t4, cp4 = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+        cfg_point("config4_logreg_100000x100", c4, t4, cp4, args.config4_chains,
+                  lambda zz: [np.zeros((zz, t4.dim)), chain_keys(0, zz)])
+        configs["config4_logreg_100000x100"]["note"] = (
+            "one GPU's shard (BASELINE shards config 4 over 2/4/8 GPUs; chains are independent, "
+            "so every rank runs this workload on its own range); sx (80 MB) streams through each "
+            "warp's shared-memory ring by bulk async copies")
         kw = dict(prebuilt.CONFIG5)
         c5, t5, cp5 = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
-        cfg_point("config5_gauss1000_cond1e4_depth15", c5, t5, cp5, 1 << 14,
+        cfg_point("config5_gauss1000_cond1e4_depth15", c5, t5, cp5, args.config5_chains,
                   lambda zz: [np.zeros((zz, t5.dim)), chain_keys(0, zz)])
 
     # cross-chain diagnostics over all ranks: the one NCCL exchange (outside the timed region)

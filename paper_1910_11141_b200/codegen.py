@@ -450,7 +450,7 @@ class _Gen:
             t = int(op["imm0"])
             cond = f"!a.exact_logpdf && lr_coop(a, a.targets[{t}])" if want_lp else f"lr_coop(a, a.targets[{t}])"
             lines.append(f"  if ({cond}) {{ __syncwarp(); warp_lr(a.targets[{t}], part_, "
-                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm, {'true' if want_lp else 'false'}); "
+                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm, {'true' if want_lp else 'false'}, a.lf_smem_per_warp); "
                          "__syncwarp(); }")
             if want_lp:
                 lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{t}], {x}, S, 1));")
@@ -714,6 +714,7 @@ class _Gen:
             pm[u] = v
             return True
 
+        alloc_a, alloc_b = [], []
         for x, y in zip(self.block_ops(a), self.block_ops(b)):
             if self.is_coop(x) or self.is_coop(y):
                 return None
@@ -724,12 +725,32 @@ class _Gen:
             for f in fields:
                 if int(x[f]) != int(y[f]):
                     return None
+            if OP.get(int(x["opcode"])) == "alloc":  # matched as sets below
+                alloc_a.append(int(x["out"]))
+                alloc_b.append(int(y["out"]))
+                continue
             if not match(int(x["out"]), int(y["out"])):
                 return None
             for j in range(int(x["nin"])):
                 if not match(int(x["in"][j]), int(y["in"][j])):
                     return None
         if int(ba["term"]) == 1 and not match(int(ba["cond"]), int(bb["cond"])):
+            return None
+        # An alloc only reserves one slot on its variable's stack, so a block's allocs are an
+        # unordered set: block B's save of (qm, qp) around a call on (qm, pm) is block A's save
+        # of (qp, qm) around a call on (qp, pp). Variables the data ops left unmapped take a
+        # free partner of the same storage (identity first) so the allocs map onto B's set.
+        images = set(pm.values())
+        for u in alloc_a:
+            if u in pm:
+                continue
+            for v in ([u] if u in alloc_b else []) + alloc_b:
+                if v not in images and match(u, v):
+                    images.add(v)
+                    break
+            else:
+                return None
+        if sorted(pm[u] for u in alloc_a) != sorted(alloc_b):
             return None
         if len(set(pm.values())) != len(pm):  # a bijection of variables
             return None
@@ -748,9 +769,13 @@ class _Gen:
             sig.setdefault(key, []).append(b)
         for group in sig.values():
             for i, a in enumerate(group):
-                if a in out or not len(self.block_ops(a)):
+                if a in out:
                     continue
+                # empty blocks (landing pads) pair only with a pad of the same successors
+                empty = not len(self.block_ops(a))
                 for b2 in group[i + 1:]:
+                    if empty and any(int(self.dp.blocks[a][f]) != int(self.dp.blocks[b2][f]) for f in ("a", "b")):
+                        continue
                     if b2 not in out and self.pair_map(a, b2) is not None:
                         out[a], out[b2] = b2, a
                         break

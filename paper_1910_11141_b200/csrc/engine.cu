@@ -811,8 +811,11 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       // DMMA logistic-regression gradients stage w the same way
       if ((op.opcode == LS_OP_GRAD || op.opcode == LS_OP_LOGPDF) && p->targets[op.imm0].kind == LS_TARGET_LOGREG &&
           p->targets[op.imm0].NT2 <= 16)
-        m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 8 * lf_stride_q(p->targets[op.imm0].dim));
+        m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, p->targets[op.imm0].n >= kLrStreamMinN
+                                                                ? lr_stream_doubles(p->targets[op.imm0].dim)
+                                                                : 8 * lf_stride_q(p->targets[op.imm0].dim));
     }
+    m->lf_smem_per_warp = (m->lf_smem_per_warp + 1) & ~1;  // 16-byte aligned per-warp areas
 #if defined(LSB_GENERATED) && LSB_GEN_STAGED
     // generated block code stages long copies through 48 rows x 32 lanes per warp
     m->lf_smem_per_warp = std::max(m->lf_smem_per_warp, 48 * 32);

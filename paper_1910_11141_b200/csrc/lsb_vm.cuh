@@ -758,9 +758,153 @@ __device__ void warp_lr_nt(const DevTarget& tg, bool part, const uint64_t* xp, u
   }
 }
 
-// grad (want_logpdf = false) or fast logpdf of a logistic-regression target, DMMA path
+// Large designs (BASELINE config 4: n = 100k points, sx = 80 MB): one warp reading sx
+// fragment by fragment keeps a few hundred bytes in flight and runs at ~1 GB/s. Instead
+// sx streams through a per-warp shared-memory ring: lane 0 issues bulk async copies
+// (cp.async.bulk, the TMA engine; completion counted in bytes on an mbarrier per stage)
+// of kLrChunk contiguous data points each, kLrStages chunks in flight, and every chunk
+// feeds BOTH GEMMs of the m-tile pass straight from shared memory — margins (B = sx^T:
+// thread (g, c) reads point g, coordinate 4ks + c) and G += s sx (B = sx: point 4kk + c,
+// coordinate 8j + g) — so sx is read once per m-tile pass instead of twice in two
+// fragment orders. Per-warp shared memory: the w tile, the ring, the barriers.
+constexpr int kLrStreamMinN = 16384;  // designs at least this tall stream (host: engine.cu)
+constexpr int kLrChunk = 16;          // data points per stage (two 8-point n-tiles)
+constexpr int kLrStages = 3;
+__host__ __device__ __forceinline__ int lr_stream_doubles(int d) {
+  return 8 * lf_stride_q(d) + kLrStages * kLrChunk * d + kLrStages + 1;  // + barriers, even
+}
+
+template <int NT2, bool LOGPDF>
+__device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+                                            double* sm) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  const unsigned mask = __ballot_sync(kFull, part);
+  const int n_act = __popc(mask);
+  if (n_act == 0) return;
+  const int d = tg.dim, n = tg.n, SQ = lf_stride_q(d), KS = (d + 3) / 4;
+  double* Xs = sm;
+  double* ring = sm + 8 * SQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kLrStages * kLrChunk * d);
+  const int MT = (n_act + 7) / 8, nch = (n + kLrChunk - 1) / kLrChunk, total = MT * nch;
+  if (lane == 0) {
+    for (int s = 0; s < kLrStages; ++s) lsbtc::mbar_init(&bars[s], 1);
+    lsbtc::fence_barrier_init();
+  }
+  __syncwarp();
+  auto issue = [&](int it) {  // lane 0: chunk it % nch into stage it % kLrStages
+    const int ch = it % nch, st = it % kLrStages;
+    const int pts = min(kLrChunk, n - ch * kLrChunk);
+    const uint32_t bytes = (uint32_t)(pts * d * 8) & ~15u;  // an odd tail word: plain load below
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    lsbtc::mbar_expect_tx(&bars[st], bytes);
+    if (bytes) lsbtc::bulk_g2s(ring + (size_t)st * kLrChunk * d, tg.P + (size_t)ch * kLrChunk * d, bytes, &bars[st]);
+  };
+  if (lane == 0)
+    for (int it = 0; it < min(kLrStages, total); ++it) issue(it);
+  const int q0 = (lane & ~3) | (c >> 1), q1 = q0 + 2;
+  const bool hi = (lane & 1) != 0;
+  double G[NT2][2];
+  double lp = 0.0;
+  int src = -1;
+  for (int it = 0; it < total; ++it) {
+    const int mt = it / nch, ch = it % nch, st = it % kLrStages;
+    if (ch == 0) {  // a new m-tile pass: stage its 8 chains' w, clear the accumulators
+      src = mtile_lane(mask, n_act, mt, g);
+      __syncwarp();
+      stage_mtile(Xs, SQ, xp, mask, n_act, mt, d);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NT2; ++j) G[j][0] = G[j][1] = 0.0;
+      lp = 0.0;
+    }
+    const int p0 = ch * kLrChunk, pts = min(kLrChunk, n - p0);
+    const double* X = ring + (size_t)st * kLrChunk * d;
+    lsbtc::mbar_wait(&bars[st], (uint32_t)((it / kLrStages) & 1));
+    if (((pts * d) & 1) && lane == 0) {
+      const size_t last = (size_t)pts * d - 1;
+      const_cast<double*>(X)[last] = __ldg(tg.P + (size_t)p0 * d + last);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < kLrChunk / 8; ++t) {
+      if (8 * t >= pts) break;  // warp-uniform
+      // margins of points 8t..8t+7 of the chunk for the m-tile's 8 chains (C layout)
+      double acc[2] = {0.0, 0.0};
+      const bool prow = 8 * t + g < pts;
+      const double* bp = X + (size_t)(8 * t + g) * d + c;
+#pragma unroll 5
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + c;
+        lsb::dmma(acc, Xs[g * SQ + k], (prow && k < d) ? bp[4 * ks] : 0.0);
+      }
+      if (LOGPDF) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (8 * t + 2 * c + e < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -acc[e]));
+        continue;
+      }
+      const double s0 = 8 * t + 2 * c < pts ? lsb::lr_sig(acc[0]) : 0.0;
+      const double s1 = 8 * t + 2 * c + 1 < pts ? lsb::lr_sig(acc[1]) : 0.0;
+      const double u0 = __shfl_sync(kFull, s0, q0), u1 = __shfl_sync(kFull, s1, q0);
+      const double v0 = __shfl_sync(kFull, s0, q1), v1 = __shfl_sync(kFull, s1, q1);
+      const double a0 = hi ? u1 : u0, a1 = hi ? v1 : v0;
+      const bool r0 = 8 * t + c < pts, r1 = 8 * t + 4 + c < pts;
+      const double* b0 = X + (size_t)(8 * t + c) * d + g;
+      const double* b1 = b0 + (size_t)4 * d;
+#pragma unroll
+      for (int j = 0; j < NT2; ++j) {
+        const bool col = 8 * j + g < d;
+        lsb::dmma(G[j], a0, (r0 && col) ? b0[8 * j] : 0.0);
+        lsb::dmma(G[j], a1, (r1 && col) ? b1[8 * j] : 0.0);
+      }
+    }
+    __syncwarp();  // every lane is done with the stage before it is refilled
+    if (lane == 0 && it + kLrStages < total) issue(it + kLrStages);
+    if (ch == nch - 1) {  // the m-tile pass is complete
+      uint64_t* dg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)dst, src < 0 ? 0 : src);
+      if (LOGPDF) {
+        lp = __dadd_rn(lp, __shfl_xor_sync(kFull, lp, 1));
+        lp = __dadd_rn(lp, __shfl_xor_sync(kFull, lp, 2));
+        if (src >= 0 && c == 0) {
+          const double ww = lsb::pairwise([&](int k) { return __dmul_rn(Xs[g * SQ + k], Xs[g * SQ + k]); }, 0, d);
+          dg[0] = f64_bits(__dsub_rn(-lp, __dmul_rn(0.5, __dadd_rn(0.0, ww))));
+        }
+      } else if (src >= 0) {
+#pragma unroll
+        for (int j = 0; j < NT2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * j + 2 * c + e;
+            if (col < d) dg[(size_t)col * 32] = f64_bits(__dsub_rn(G[j][e], Xs[g * SQ + col]));
+          }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int s = 0; s < kLrStages; ++s)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(lsbtc::smem_u32(&bars[s])) : "memory");
+  __syncwarp();
+}
+
+// grad (want_logpdf = false) or fast logpdf of a logistic-regression target, DMMA path;
+// sm_doubles: the warp's shared-memory scratch (tall designs stream through it)
 __device__ inline void warp_lr(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst, double* Xs,
-                               bool want_logpdf) {
+                               bool want_logpdf, int sm_doubles) {
+  if (tg.n >= kLrStreamMinN && sm_doubles >= lr_stream_doubles(tg.dim)) {
+    switch (tg.NT2) {
+#define LSB_LRS_CASE(K)                                                        \
+  case K:                                                                      \
+    if (want_logpdf) warp_lr_stream<K, true>(tg, part, xp, dst, Xs);           \
+    else warp_lr_stream<K, false>(tg, part, xp, dst, Xs);                      \
+    return;
+      LSB_LRS_CASE(1) LSB_LRS_CASE(2) LSB_LRS_CASE(3) LSB_LRS_CASE(4) LSB_LRS_CASE(5) LSB_LRS_CASE(6)
+      LSB_LRS_CASE(7) LSB_LRS_CASE(8) LSB_LRS_CASE(9) LSB_LRS_CASE(10) LSB_LRS_CASE(11) LSB_LRS_CASE(12)
+      LSB_LRS_CASE(13) LSB_LRS_CASE(14) LSB_LRS_CASE(15) LSB_LRS_CASE(16)
+#undef LSB_LRS_CASE
+      default: break;
+    }
+  }
   switch (tg.NT2) {
 #define LSB_LR_CASE(K)                                                   \
   case K:                                                                \
@@ -777,7 +921,7 @@ __device__ inline void warp_lr(const DevTarget& tg, bool part, const uint64_t* x
 
 __device__ inline void warp_lr_grad(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
                                     double* Xs) {
-  warp_lr(tg, part, xp, dst, Xs, false);
+  warp_lr(tg, part, xp, dst, Xs, false, 0);
 }
 
 // LR gradients take the DMMA path when the warp's scratch holds an 8-chain tile of w
@@ -1203,7 +1347,7 @@ __device__ __forceinline__ bool exec_block(const VMArgs& a, const Lane& ln, int 
         __syncwarp();
         if (a.targets[op.imm0].kind == LS_TARGET_LOGREG)
           warp_lr(a.targets[op.imm0], part, part ? ln.in(op, 0) : nullptr, dst, lf_smem,
-                  op.opcode == LS_OP_LOGPDF);
+                  op.opcode == LS_OP_LOGPDF, a.lf_smem_per_warp);
         else
           warp_gauss(a.targets[op.imm0], staged_B(a, op.imm0), part, part ? ln.in(op, 0) : nullptr, dst,
                      op.opcode == LS_OP_LOGPDF, lf_smem, a.lf_smem_per_warp);

@@ -35,14 +35,19 @@ TEST_NUTS = [
 # single-leaf programs (entry = leapfrog) whose fused superblock the per-step test checks
 # against the reference's leapfrog vectors (tests/golden/leapfrog.npz)
 LEAPFROG = [(2, 1), (2, 4), (100, 1), (100, 4)]
-# BASELINE configs 3 and 5 as bench.py measures them (their own bench-line objects)
-CONFIG3 = dict(n=1000, d=25, seed=0, step_size=0.05, leaf_steps=4, max_depth=10, iterations=5)
+# BASELINE configs 3, 4 and 5 as bench.py measures them (their own bench-line objects); config 3
+# runs 20 iterations: with 5 the launch is the tail of the few chains that build depth-10 trees
+CONFIG3 = dict(n=1000, d=25, seed=0, step_size=0.05, leaf_steps=4, max_depth=10, iterations=20)
+# BASELINE config 4: the 100k x 100 design (sx = 80 MB streams through shared memory), the
+# reference's own measured setting (depth 10, step 0.004, 2 iterations)
+CONFIG4 = dict(n=100_000, d=100, seed=0, step_size=0.004, leaf_steps=4, max_depth=10, iterations=2)
 CONFIG5 = dict(dim=1000, rho=9999 / 10999, step_size=0.02, leaf_steps=4, max_depth=15, iterations=2)
 # the headline target with dispersed starting points and a smaller step: trees of varying depth,
 # so lanes of a warp diverge (the case program-counter autobatching exists for)
 DISPERSED = dict(dim=100, rho=0.5, step_size=0.1, leaf_steps=4, max_depth=10, iterations=10)
 # logistic-regression cases (DMMA two-GEMM gradient): gradient-only programs and one NUTS run
-LR_GRAD = [(200, 5, 7), (1000, 25, 0)]
+# (the two tall designs take the streamed path: n >= kLrStreamMinN; 20001 x 7 ends on an odd word)
+LR_GRAD = [(200, 5, 7), (1000, 25, 0), (20001, 7, 3), (100_000, 100, 0)]
 LR_NUTS = dict(n=200, d=5, seed=7, step_size=0.1, leaf_steps=2, max_depth=5, iterations=3)
 
 
@@ -85,6 +90,9 @@ def specs():
     kw = dict(CONFIG3)
     _, t, cp = lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
     out.append(("config3", cp, [VType("f64", t.dim), I64]))
+    kw = dict(CONFIG4)
+    _, t, cp = lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    out.append(("config4", cp, [VType("f64", t.dim), I64]))
     kw = dict(CONFIG5)
     dim, rho = kw.pop("dim"), kw.pop("rho")
     _, _, cp = nuts(dim, rho, **kw)

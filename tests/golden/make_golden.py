@@ -12,6 +12,9 @@ only) and records, with the numpy/OpenBLAS build of this container:
 * single-leaf leapfrog vectors (entry='leapfrog')         (test_acceptance.py:294-312)
 * logistic-regression logpdf/grad values                  (workloads.py:216-228)
 * local-static engine schedules + gradient utilisation     (local_exec.py:142-193)
+* long runs for the in-distribution checks: the reference's own chains (samples) of a
+  5-d correlated gaussian and of logistic regression 200x5, plus the reference's moment
+  ground truth (reference_moments / moment_fn, workloads.py:126-128, 230-249)
 
 The GPU box has no /root/reference; tests read only these files.
 Usage: python tests/golden/make_golden.py
@@ -192,6 +195,35 @@ def local_runs() -> tuple[dict, dict]:
     return arrays, meta
 
 
+# in-distribution cases: name, target factory, NutsConfig kwargs, z, key seed
+DIST_CASES = [
+    ("dist_g5", lambda: R.correlated_gaussian(5, 0.9),
+     dict(step_size=0.2, leaf_steps=4, max_depth=8, iterations=200, seed=0), 128, 5),
+    ("dist_lr200x5", lambda: R.logistic_regression(200, 5, seed=7),
+     dict(step_size=0.1, leaf_steps=4, max_depth=8, iterations=150, seed=0), 64, 6),
+]
+
+
+def dist_runs() -> tuple[dict, dict]:
+    """Long reference runs (pc_vm.run from q0 = 0): the chains themselves (workloads.py:477
+    chain_array layout) and the target's moment ground truth, for distribution checks of
+    device runs on other seeds (tests/test_distribution.py)."""
+    arrays, meta = {}, {}
+    for name, make, kw, z, seed in DIST_CASES:
+        t = make()
+        cfg = R.NutsConfig(**kw)
+        cp = R.compile_program(R.compile_source(R.nuts_lite_source(cfg, t), "nuts_main"))
+        key = np.random.default_rng(seed).integers(0, 2**31, size=z).astype(np.int64)
+        out, tr = R.pc_vm.run(cp, [np.zeros((z, t.dim)), key], depth=cfg.min_stack_depth)
+        arrays[f"{name}_key"] = key
+        arrays[f"{name}_samples"] = R.workloads.chain_array(out, cfg, t.dim)
+        mean, cov = t.reference_moments()
+        arrays[f"{name}_mean"], arrays[f"{name}_cov"] = np.asarray(mean), np.asarray(cov)
+        meta[name] = {"dim": t.dim, "config": kw, "z": z, "key_seed": seed, "target": t.name,
+                      "useful_grads": int(sum(s.active * s.prims.get(t.grad, 0) for s in tr.steps))}
+    return arrays, meta
+
+
 def Rir_index(cp, label: str) -> int:
     return cp.labels.index(label)
 
@@ -226,6 +258,13 @@ def logreg_values() -> dict:
 
 
 def main():
+    if sys.argv[1:] == ["dist"]:  # only the long runs (a few minutes), merged into golden.json
+        meta = json.loads((OUT / "golden.json").read_text())
+        arrays, meta["dist"] = dist_runs()
+        np.savez_compressed(OUT / "dist_runs.npz", **arrays)
+        (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
+        print("wrote dist fixtures to", OUT)
+        return
     meta = {"env": env(), "generator": "tests/golden/make_golden.py",
             "reference": "/root/reference/pkg/src/lockstep"}
     np.savez_compressed(OUT / "rng_kat.npz", **rng_grid())
@@ -242,6 +281,8 @@ def main():
     meta["local"] = lmeta
     np.savez_compressed(OUT / "leapfrog.npz", **leapfrog_vectors())
     np.savez_compressed(OUT / "logreg.npz", **logreg_values())
+    arrays, meta["dist"] = dist_runs()
+    np.savez_compressed(OUT / "dist_runs.npz", **arrays)
     (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print("wrote fixtures to", OUT)
 

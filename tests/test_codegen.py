@@ -1,8 +1,8 @@
 """Program-specialised block code (codegen.py) on CPU: what gets generated, not run.
 
 * blocks with identical code on different variables (the two direction variants of
-  NUTS-lite's tree calls and landing pads) are paired into one warp step, each lane
-  on its own block's storage;
+  NUTS-lite's tree calls, frame saves and landing pads) are paired into one warp step,
+  each lane on its own block's storage; a block's allocs match as a set;
 * generation is deterministic and thread-safe (the prebuilt libraries are looked up
   by the hash of the generated text, and build_all generates on several threads).
 """
@@ -32,6 +32,13 @@ def test_direction_variants_are_paired():
     assert named["nuts_main.b11"] == "nuts_main.b12"
     assert named["nuts_main.b14"] == "nuts_main.b15"
     assert named["build_tree.b10"] == "build_tree.b11"
+    # the recursive calls' frame saves: the same stacks allocated, the call on (qp, pp) vs (qm, pm)
+    assert named["build_tree.b7"] == "build_tree.b8"
+    # empty landing pads pair only with a pad of the same successor
+    assert named["nuts_main.r19"] == "nuts_main.r20"
+    for a, b in pairs.items():
+        if not len(codegen._Gen(dp).block_ops(a)):
+            assert int(dp.blocks[a]["a"]) == int(dp.blocks[b]["a"])
     assert all(pairs[b] == a for a, b in pairs.items())  # symmetric, disjoint
     src = codegen.generate(dp)
     assert "const bool sB_ = pc_ == 12;" in src and "case 12: return gb_11(" in src
@@ -50,6 +57,22 @@ def test_pair_map_rejects_different_code():
     a, b = cp.labels.index("nuts_main.b11"), cp.labels.index("nuts_main.b12")
     pm = g.pair_map(a, b)
     assert pm is not None and len(set(pm.values())) == len(pm)
+
+
+def test_alloc_sets_map_onto_each_other():
+    """b7/b8 save the same eight stacks; the pair's variable map sends A's allocated set
+    onto B's and stays a bijection, while the call arguments keep their positional map."""
+    cp, dp = _bench_dp()
+    g = codegen._Gen(dp)
+    a, b = cp.labels.index("build_tree.b7"), cp.labels.index("build_tree.b8")
+    pm = g.pair_map(a, b)
+    name = dp.var_names
+    by = {name[u]: name[v] for u, v in pm.items()}
+    assert by["build_tree.qp"] == "build_tree.qm" and by["build_tree.pp"] == "build_tree.pm"
+    assert by["build_tree.qm"] == "build_tree.qp" and by["build_tree.pm"] == "build_tree.pp"
+    allocs = lambda blk: sorted(int(o["out"]) for o in g.block_ops(blk) if codegen.OP.get(int(o["opcode"])) == "alloc")
+    assert sorted(pm[u] for u in allocs(a)) == allocs(b)
+    assert len(set(pm.values())) == len(pm)
 
 
 def test_generation_is_deterministic_across_threads():

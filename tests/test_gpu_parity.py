@@ -413,6 +413,26 @@ def test_warp_engine_logreg_dmma_gradient(codegen):
     assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
 
 
+def test_config4_tall_logreg_lanes_exact_on_a_sample():
+    """BASELINE config 4 (logistic regression on a 100k x 100 design; sx = 80 MB streams
+    through each warp's shared-memory ring by bulk async copies): 40 chains of the bench's
+    program through its specialised library — every lane's pc trace equals the oracle's
+    (tree depths, U-turns, accepts) and the chains agree within CHAIN_RTOL."""
+    from paper_1910_11141_b200 import prebuilt
+
+    kw = dict(prebuilt.CONFIG4)
+    cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    z = 40
+    ins = [np.zeros((z, t.dim)), np.arange(z, dtype=np.int64) * 7919 + 11]
+    ref = oracle_run(cp, ins, cfg.min_stack_depth, lane_traces=True)
+    for exact in (True, False):
+        got, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen="cached",
+                          exact_logpdf=exact, lane_trace_cap=1 << 16, return_machine=True)
+        for lane, seq in enumerate(m.lane_traces()):
+            assert np.array_equal(seq, ref.lane_blocks[lane]), (exact, lane)
+        assert (np.abs(got - ref.output) / np.maximum(np.abs(ref.output), 1.0)).max() < CHAIN_RTOL
+
+
 def test_warp_engine_logreg_fast_logpdf():
     """Fast mode (exact_logpdf=False): the fused DMMA logistic-regression logpdf agrees with
     the reference formula (workloads.py:216-219) to 1e-12 relative."""

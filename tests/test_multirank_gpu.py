@@ -15,12 +15,17 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-Z = 3000
+# (program, chains): NUTS-lite on the 5-d gaussian, and BASELINE config 4 (logistic
+# regression on the 100k x 100 design, its sx streamed by every warp) on a small batch
+CASES = [("gauss5", 3000), ("config4", 48)]
 
 
-def _program():
+def _program(name="gauss5"):
     from paper_1910_11141_b200 import prebuilt
 
+    if name == "config4":
+        kw = dict(prebuilt.CONFIG4)
+        return prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
     kw = dict(prebuilt.TEST_NUTS[2])  # d = 5, T = 4, depth 8
     return prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
 
@@ -31,12 +36,12 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, name, Z):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1910_11141_b200 import distributed as D
 
-    cfg, t, cp = _program()
+    cfg, t, cp = _program(name)
     out, lo, hi, tr = D.run_shard(cp, np.zeros((Z, t.dim)), z_total=Z, rank=rank, world=world,
                                   depth=cfg.min_stack_depth, device=0, engine="warp", codegen="cached",
                                   exact_logpdf=False, schedule="priority")
@@ -46,18 +51,19 @@ def _rank(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_ranks_on_one_gpu_equal_the_single_rank_run():
+@pytest.mark.parametrize("name,Z", CASES)
+def test_two_ranks_on_one_gpu_equal_the_single_rank_run(name, Z):
     from paper_1910_11141_b200 import distributed as D
     import paper_1910_11141_b200 as L
 
-    cfg, t, cp = _program()
+    cfg, t, cp = _program(name)
     single, _ = L.run(cp, [np.zeros((Z, t.dim)), D.chain_keys(0, Z)], depth=cfg.min_stack_depth,
                       engine="warp", codegen="cached", exact_logpdf=False, schedule="priority", device=0)
     ref = D.diagnostics(torch.from_numpy(single.reshape(Z, cfg.iterations, t.dim).copy()))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, name, Z)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda r: r[0])

@@ -18,8 +18,16 @@ z = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 cg = (sys.argv[2] != "0") if len(sys.argv) > 2 else True
 sched = sys.argv[3] if len(sys.argv) > 3 else "priority"
 prec = sys.argv[4] if len(sys.argv) > 4 else "fp64"
-kw = dict(prebuilt.BENCH)
-cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+prog = os.environ.get("BP_PROGRAM", "bench")
+if prog == "config3":
+    kw = dict(prebuilt.CONFIG3)
+    cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+elif prog == "config5":
+    kw = dict(prebuilt.CONFIG5)
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+else:
+    kw = dict(prebuilt.BENCH)
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
 q0 = np.zeros((z, t.dim))
 key = np.arange(z, dtype=np.int64) * 7919 + 11
 m = L.init_machine(cp, [q0, key], depth=cfg.min_stack_depth, engine="warp", optimize=True,
@@ -32,7 +40,8 @@ steps, active = m._h.block_totals(nb)
 cyc = m._h.block_cycles(nb)
 ops = np.array([int(b["op_count"]) for b in m._dp.blocks])
 groups = max(1, (z + 31) // 32)
-print(f"kernel {st.kernel_ms:.1f} ms, {st.useful_grads / st.kernel_ms / 1e3:.1f} M grads/s, "
+print(f"{prog}: kernel {st.kernel_ms:.1f} ms, {st.useful_grads / st.kernel_ms / 1e3:.1f} M grads/s, "
+      f"grad utilisation {st.useful_grads / max(st.launched_grads, 1):.3f}, "
       f"steps/warp {steps.sum() / groups:.0f}, cycles/warp {cyc.sum() / groups / 1e6:.2f} M")
 for b in np.argsort(-cyc)[:20]:
     print(f"{b:3d} {cp.labels[b]:18s} steps/warp {steps[b] / groups:7.1f} lanes/step "

@@ -1,6 +1,6 @@
 """One BASELINE config point on the warp engine + prebuilt library (dev tool, GPU).
 
-usage: python tools/config_point.py config3|config5|dispersed [chains] [fp64|fp32]
+usage: python tools/config_point.py config3|config4|config5|dispersed [chains] [fp64|fp32]
 """
 import os
 import sys
@@ -17,6 +17,10 @@ z = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 14
 prec = sys.argv[3] if len(sys.argv) > 3 else "fp64"
 if which == "config3":
     kw = dict(prebuilt.CONFIG3)
+    cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
+    q0 = np.zeros((z, t.dim))
+elif which == "config4":
+    kw = dict(prebuilt.CONFIG4)
     cfg, t, cp = prebuilt.lr_nuts(kw.pop("n"), kw.pop("d"), kw.pop("seed"), **kw)
     q0 = np.zeros((z, t.dim))
 elif which == "config5":
