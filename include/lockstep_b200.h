@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define LS_ABI_VERSION 2
+#define LS_ABI_VERSION 3
 
 /* ---- status codes ---------------------------------------------------------- */
 enum {
@@ -171,6 +171,9 @@ typedef struct {
                              DMMA target contractions and fused superblocks; `ctas`
                              then caps the groups at 4 x ctas */
   int32_t flags;          /* LS_MF_* bits                                             */
+  int32_t group_trace_cap; /* warp engine, >0: every group records its first cap steps
+                             (block, active lanes) — the reference's per-step schedule
+                             trace (metrics.py:36-41) per 32-lane group             */
 } ls_machine_opts;
 
 /* ls_machine_opts.flags */
@@ -252,6 +255,11 @@ int ls_read_pointers(ls_machine* m, int32_t var, int64_t* host, int64_t z);
 int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count);
 /* per-chain block sequences: blocks [z][cap], lens [z] (a len > cap was truncated) */
 int ls_lane_trace_fetch(ls_machine* m, int32_t* blocks, int32_t* lens, int64_t cap);
+/* warp engine step records per group (reference ScheduleTrace.record, metrics.py:36-37, one
+   trace per 32-lane group): recs [groups][cap] = block | active << 16, a paired step (two
+   blocks of identical code on different variables) as two records; lens [groups] (> cap:
+   truncated). Needs group_trace_cap > 0 at create; groups from ls_machine_info. */
+int ls_group_trace_fetch(ls_machine* m, int32_t* recs, int32_t* lens, int64_t cap);
 int ls_machine_sync(ls_machine* m);
 /* where and how a machine runs: CUDA device, schedule groups, lanes per group */
 int ls_machine_info(const ls_machine* m, int32_t* device, int32_t* groups, int32_t* lanes_per_group);

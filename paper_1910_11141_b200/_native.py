@@ -40,7 +40,7 @@ class ProgramDesc(C.Structure):
 class MachineOpts(C.Structure):
     _fields_ = [("sched", C.c_int32), ("lanes_per_cta", C.c_int32), ("ctas", C.c_int32),
                 ("trace", C.c_int32), ("exact_logpdf", C.c_int32), ("lane_trace_cap", C.c_int32),
-                ("warp_groups", C.c_int32), ("flags", C.c_int32)]
+                ("warp_groups", C.c_int32), ("flags", C.c_int32), ("group_trace_cap", C.c_int32)]
 
 
 class Status(C.Structure):
@@ -80,6 +80,7 @@ _SIGS = {
     "ls_read_pointers": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_int64], C.c_int),
     "ls_read_pc_stack": ([C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_lane_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
+    "ls_group_trace_fetch": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64], C.c_int),
     "ls_machine_sync": ([C.c_void_p], C.c_int),
     "ls_machine_destroy": ([C.c_void_p], C.c_int),
     "ls_rng_uniform": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
@@ -239,7 +240,7 @@ class MachineHandle:
     def __init__(self, program: Program, z: int, depth: int, *, sched: str = "min_pc",
                  lanes_per_cta: int = 0, ctas: int = 0, trace: bool = False,
                  exact_logpdf: bool = True, lane_trace_cap: int = 0, warp_groups: bool = False,
-                 stage_targets: bool = True, precision: str = "fp64"):
+                 stage_targets: bool = True, precision: str = "fp64", group_trace_cap: int = 0):
         if sched not in SCHED:
             raise ValueError(f"unknown schedule '{sched}'")
         self.program = program
@@ -248,13 +249,15 @@ class MachineHandle:
         self.depth = depth
         opts = MachineOpts(SCHED[sched], lanes_per_cta, ctas, int(trace), int(exact_logpdf),
                            int(lane_trace_cap), int(warp_groups),
-                           (0 if stage_targets else MF_NO_STAGE) | (MF_FP32 if precision == "fp32" else 0))
+                           (0 if stage_targets else MF_NO_STAGE) | (MF_FP32 if precision == "fp32" else 0),
+                           int(group_trace_cap))
         if precision not in PRECISIONS:
             raise ValueError(f"unknown precision '{precision}' (one of {PRECISIONS})")
         if precision == "fp32" and not warp_groups:
             raise ValueError("the fp32 arm runs on the warp engine (engine='warp')")
         self.precision = precision
         self.lane_trace_cap = int(lane_trace_cap)
+        self.group_trace_cap = int(group_trace_cap)
         self.warp_groups = bool(warp_groups)
         self._host_out: np.ndarray | None = None
         h = C.c_void_p()
@@ -384,6 +387,16 @@ class MachineHandle:
         if (lens > cap).any():
             raise ValueError(f"lane trace truncated: raise lane_trace_cap above {int(lens.max())}")
         return [blocks[i, :lens[i]].copy() for i in range(self.z)]
+
+    def group_traces(self) -> list[np.ndarray]:
+        """Warp engine: every group's step records (block | active << 16), in step order."""
+        cap, groups = self.group_trace_cap, self.groups
+        recs = np.empty((groups, cap), np.int32)
+        lens = np.empty(groups, np.int32)
+        self._c(self.lib.ls_group_trace_fetch(self.handle, _ptr(recs), _ptr(lens), cap))
+        if (lens > cap).any():
+            raise ValueError(f"group trace truncated: raise group_trace_cap above {int(lens.max())}")
+        return [recs[g, :lens[g]].copy() for g in range(groups)]
 
     def sync(self) -> None:
         self._c(self.lib.ls_machine_sync(self.handle))

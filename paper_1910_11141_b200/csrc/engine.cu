@@ -344,6 +344,14 @@ __device__ __forceinline__ void warp_group_run(const VMArgs& a, double* lf_smem)
     if (lane == 0) {
       const int grads = __ldg(&a.blocks[b].grads);
       const int count_b = count - count_pb;
+      if (a.gtrace != nullptr) {  // the group's schedule trace (reference ScheduleTrace.record)
+        int n = a.gtrace_len[g];
+        int* rec = a.gtrace + (size_t)g * a.gtrace_cap;
+        if (count_b && n < a.gtrace_cap) rec[n] = b | (count_b << 16);
+        n += count_b ? 1 : 0;
+        if (count_pb && n < a.gtrace_cap) rec[n] = pb | (count_pb << 16);
+        a.gtrace_len[g] = n + (count_pb ? 1 : 0);
+      }
       atomicAdd((unsigned long long*)&bsteps[b], 1ull);
       atomicAdd((unsigned long long*)&bactive[b], (unsigned long long)count_b);
       useful += (unsigned long long)count_b * (unsigned long long)grads;
@@ -502,6 +510,9 @@ struct ls_machine {
   int* lane_trace = nullptr;
   int* lane_trace_len = nullptr;
   int lane_trace_cap = 0;
+  int* gtrace = nullptr;
+  int* gtrace_len = nullptr;
+  int gtrace_cap = 0;
   bool started = false;
   bool warp = false;
   bool refill = false;
@@ -600,6 +611,7 @@ static VMArgs make_args(ls_machine* m, long long max_steps) {
   a.stage_doubles = m->stage_doubles;
   a.stage_src = m->stage_target >= 0 ? p->targets[m->stage_target].B1 : nullptr;
   a.lane_trace = m->lane_trace; a.lane_trace_len = m->lane_trace_len; a.lane_trace_cap = m->lane_trace_cap;
+  a.gtrace = m->gtrace; a.gtrace_len = m->gtrace_len; a.gtrace_cap = m->gtrace_cap;
   a.fault = m->fault; a.abort_flag = m->flags + 0; a.paused = m->flags + 1;
   a.bkey = m->bkey;
   a.wg = m->fp32 ? 1 : 0;
@@ -733,7 +745,7 @@ int ls_machine_destroy(ls_machine* m) {
   cudaFree(m->group_steps); cudaFree(m->group_done); cudaFree(m->trace_block);
   cudaFree(m->trace_active); cudaFree(m->trace_n); cudaFree(m->blk_steps);
   cudaFree(m->blk_active); cudaFree(m->blk_cycles); cudaFree(m->fault); cudaFree(m->flags);
-  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len); cudaFree(m->bkey); cudaFree(m->tc_img);
+  cudaFree(m->lane_trace); cudaFree(m->lane_trace_len); cudaFree(m->gtrace); cudaFree(m->gtrace_len); cudaFree(m->bkey); cudaFree(m->tc_img);
   if (m->ev0) cudaEventDestroy(m->ev0);
   if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->stream) cudaStreamDestroy(m->stream);
@@ -755,6 +767,7 @@ static int reset_state(ls_machine* m) {
   CK(cudaMemsetAsync(m->flags, 0, 4 * sizeof(int), m->stream));
   CK(cudaMemsetAsync(m->trace_n, 0, sizeof(long long), m->stream));
   if (m->lane_trace_len) CK(cudaMemsetAsync(m->lane_trace_len, 0, (size_t)m->z * sizeof(int), m->stream));
+  if (m->gtrace_len) CK(cudaMemsetAsync(m->gtrace_len, 0, (size_t)m->groups * sizeof(int), m->stream));
   {
     const FaultRec f0{~0ull, 0, 0, 0, 0, -1};
     std::vector<FaultRec> fr((size_t)m->groups, f0);
@@ -994,6 +1007,17 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
   if (m->opts.lane_trace_cap > 0) {
     m->lane_trace_cap = m->opts.lane_trace_cap;
     if ((rc = dalloc(&m->lane_trace, (size_t)z * m->lane_trace_cap)) || (rc = dalloc(&m->lane_trace_len, (size_t)z))) {
+      ls_machine_destroy(m);
+      return rc;
+    }
+  }
+  if (m->opts.group_trace_cap > 0) {
+    if (!m->warp) {
+      ls_machine_destroy(m);
+      return fail(LS_EINVAL, "group traces are recorded by the warp engine (warp_groups = 1)");
+    }
+    m->gtrace_cap = m->opts.group_trace_cap;
+    if ((rc = dalloc(&m->gtrace, (size_t)groups * m->gtrace_cap)) || (rc = dalloc(&m->gtrace_len, (size_t)groups))) {
       ls_machine_destroy(m);
       return rc;
     }
@@ -1302,6 +1326,16 @@ int ls_read_pc_stack(ls_machine* m, int32_t* host, int64_t count) {
   CK(cudaMemcpy(raw.data(), m->pcs, raw.size() * sizeof(int), cudaMemcpyDeviceToHost));
   for (int s = 0; s <= m->depth; ++s)
     for (long long l = 0; l < m->z; ++l) host[(size_t)s * m->z + l] = raw[(size_t)s * m->lanes + l];
+  return LS_OK;
+}
+
+int ls_group_trace_fetch(ls_machine* m, int32_t* recs, int32_t* lens, int64_t cap) {
+  if (!m || !m->gtrace) return fail(LS_EINVAL, "machine was created without group traces");
+  if (cap != m->gtrace_cap) return fail(LS_EINVAL, "group trace capacity mismatch");
+  CK(cudaSetDevice(m->device));
+  CK(cudaStreamSynchronize(m->stream));
+  CK(cudaMemcpy(recs, m->gtrace, (size_t)m->groups * cap * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(lens, m->gtrace_len, (size_t)m->groups * sizeof(int), cudaMemcpyDeviceToHost));
   return LS_OK;
 }
 

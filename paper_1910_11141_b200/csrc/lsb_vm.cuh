@@ -115,6 +115,9 @@ struct VMArgs {
   int* lane_trace;
   int* lane_trace_len;
   int lane_trace_cap;
+  int* gtrace;                  // warp engine: [groups][gtrace_cap] block | active << 16
+  int* gtrace_len;              // [groups] records written (may exceed the cap)
+  int gtrace_cap;
   FaultRec* fault;              // [n_groups] one fault slot per group
   int* abort_flag;
   int* paused;

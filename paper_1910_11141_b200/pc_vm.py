@@ -183,6 +183,39 @@ class Machine:
         """Each lane's executed block sequence (needs lane_trace_cap > 0 at init)."""
         return self._h.lane_traces()
 
+    def group_traces(self) -> list[ScheduleTrace]:
+        """Warp engine (group_trace_cap > 0 at init): one reference ScheduleTrace per
+        32-lane group — StepRecord(block label, active lanes, prims) per step and the
+        per-variable stack-op counts (reference metrics.py:29-41), so utilization(),
+        compare() and trace_to_json() apply per group. Fused superblocks carry their
+        function's gradient count; a paired step appears as two records."""
+        from .lowering import grad_names
+
+        dp = self._dp
+        gnames = grad_names()
+        prims = []
+        for b, p in enumerate(dp.block_prims):
+            p = {k: v for k, v in p.items() if k not in gnames}
+            g = int(dp.blocks["grads"][b])
+            if g:  # the device's count (a fused superblock does its function's gradients)
+                fn = self.labels[b].split(".", 1)[0]
+                names = [k for k in dp.block_prims[b] if k in gnames] or \
+                        [k for c, q in enumerate(dp.block_prims) if self.labels[c].split(".", 1)[0] == fn
+                         for k in q if k in gnames]
+                if names:
+                    p[names[0]] = g
+            prims.append(p)
+        out = []
+        for recs in self._h.group_traces():
+            tr = ScheduleTrace(engine="pc", z=32)
+            for r in recs:
+                b, act = int(r) & 0xffff, int(r) >> 16
+                tr.record(self.labels[b], act, prims[b])
+                for var, kind in dp.block_stack_ops[b]:
+                    tr.record_stack_op(var, kind)
+            out.append(tr)
+        return out
+
     @property
     def useful_grads(self) -> int:
         """Sum over steps of active lanes x grad invocations (the headline unit)."""
@@ -270,7 +303,7 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
                  optimize: bool = False, exact_logpdf: bool = True,
                  lane_trace_cap: int = 0, engine: str = "auto",
                  codegen: bool | str = False, reuse: bool = False, device: int | None = None,
-                 precision: str = "fp64") -> Machine:
+                 precision: str = "fp64", group_trace_cap: int = 0) -> Machine:
     """Allocate device storage and seed the batch (reference pc_vm.py:140-213).
 
     Data stacks get `depth` slots with one live slot per lane; inputs land in
@@ -293,6 +326,8 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     its LOCAL_RANK; None = the library's current device, 0 by default).
     schedule: block-selection rule (schedule.SCHEDULES): "min_pc" (reference),
     "most_populated", "local" (paper Alg. 1) or "priority" (throughput).
+    group_trace_cap (warp engine): record each 32-lane group's first steps as the
+    reference's per-step schedule trace (Machine.group_traces).
     """
     if mode not in ("masked", "gather"):
         raise ValueError(f"unknown mode '{mode}'")
@@ -333,7 +368,8 @@ def init_machine(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "
     lanes = z if exact else (32 if kind == "warp" else int(lanes_per_group))
     mopts = dict(sched=schedule, lanes_per_cta=int(lanes_per_group) if kind == "cta" else 0,
                  ctas=groups, trace=exact and trace is not None, exact_logpdf=exact_logpdf,
-                 lane_trace_cap=lane_trace_cap, warp_groups=(kind == "warp"), precision=precision)
+                 lane_trace_cap=lane_trace_cap, warp_groups=(kind == "warp"), precision=precision,
+                 group_trace_cap=group_trace_cap)
     mkey = (pkey, z, depth, tuple(sorted(mopts.items())))
     handle = _MACHINE_CACHE.pop(mkey, None) if reuse else None
     if handle is not None and handle.program is program:
@@ -460,7 +496,7 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
         schedule: str = "min_pc", lanes_per_group: int | None = None, groups: int = 0,
         optimize: bool | None = None, exact_logpdf: bool = True, lane_trace_cap: int = 0,
         engine: str = "auto", codegen: bool | str = False, return_machine: bool = False,
-        device: int | None = None, precision: str = "fp64"):
+        device: int | None = None, precision: str = "fp64", group_trace_cap: int = 0):
     """Execute a compiled program on the B200; returns (outputs, trace)."""
     arrays = [a if isinstance(a, np.ndarray) else batch(a) for a in inputs]
     z = arrays[0].shape[0] if arrays else 0
@@ -473,7 +509,8 @@ def run(compiled: CompiledProgram, inputs, *, depth: int, mode: str = "masked",
     m = init_machine(compiled, arrays, depth=depth, mode=mode, trace=tr, schedule=schedule,
                      lanes_per_group=lanes_per_group, groups=groups, optimize=optimize,
                      exact_logpdf=exact_logpdf, lane_trace_cap=lane_trace_cap, engine=engine,
-                     codegen=codegen, reuse=reuse, device=device, precision=precision)
+                     codegen=codegen, reuse=reuse, device=device, precision=precision,
+                     group_trace_cap=group_trace_cap)
     if m.engine == "warp" and observer is None and not debug and not return_machine:
         # output rows go straight to a pinned host buffer while the run executes (not for
         # a machine handed back: its device output must stay valid for later reads)

@@ -22,7 +22,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(_native._SIGS), "ctypes signatures must cover the header exactly"
-    assert lib.ls_abi_version() == 2
+    assert lib.ls_abi_version() == 3
 
 
 def test_struct_layouts_match_header():

@@ -552,6 +552,55 @@ def test_device_dot_bit_exact_on_reference_rows(engine):
         assert got.tobytes() == np.array([r[2] for r in rows]).tobytes(), n
 
 
+@pytest.mark.parametrize("case", ["nuts_d5", "nuts_d100", "nuts_d3m"])
+def test_warp_engine_group_trace_is_the_reference_trace(golden_meta, case):
+    """Tracing on the throughput engine: a batch of <= 32 chains is one warp group; with the
+    reference's rule and program (min_pc, no fusion, interpreter) its group trace is the
+    reference's own ScheduleTrace step for step — block, active lanes — with the same
+    per-variable stack-op counts, and it round-trips the reference's JSON wire format."""
+    from paper_1910_11141_b200.reference import metrics as RM
+
+    meta = golden_meta["nuts"][case]
+    g = load_npz("nuts_runs.npz")
+    t = L.correlated_gaussian(meta["dim"], meta["rho"])
+    cfg = L.NutsConfig(**meta["config"])
+    cp = L.compile_program(L.compile_source(L.nuts_lite_source(cfg, t), "nuts_main"))
+    ins = [np.zeros((meta["z"], meta["dim"])), g[f"{case}_key"]]
+    out, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen=False, optimize=False,
+                      schedule="min_pc", group_trace_cap=1 << 16, return_machine=True)
+    np.testing.assert_allclose(out, g[f"{case}_out"], rtol=CHAIN_RTOL, atol=CHAIN_RTOL)
+    trs = m.group_traces()
+    assert len(trs) == 1
+    want = [tuple(int(v) for v in x) for x in g[f"{case}_steps"]]
+    assert [(cp.labels.index(s.block), s.active) for s in trs[0].steps] == want
+    assert trs[0].stack_ops == meta["stack_ops"]
+    back = RM.trace_from_json(RM.trace_to_json(trs[0]))
+    assert back.steps == trs[0].steps and back.stack_ops == trs[0].stack_ops
+    assert RM.utilization(trs[0], {t.grad}) == pytest.approx(
+        meta["useful_grads"] / (meta["z"] * sum(s.prims.get(t.grad, 0) for s in trs[0].steps)))
+
+
+def test_group_traces_account_for_every_gradient():
+    """The benchmarked library (fused superblocks, paired blocks, priority schedule) on 96
+    chains = three groups: the group traces' useful gradient invocations add up to the run's
+    useful-gradient count, and each group's utilization is in (0, 1]."""
+    from paper_1910_11141_b200 import prebuilt
+    from paper_1910_11141_b200.reference import metrics as RM
+
+    kw = dict(prebuilt.BENCH)
+    cfg, t, cp = prebuilt.nuts(kw.pop("dim"), kw.pop("rho"), **kw)
+    z = 96
+    ins = [np.zeros((z, t.dim)), np.arange(z, dtype=np.int64) * 7919 + 11]
+    _, _, m = L.run(cp, ins, depth=cfg.min_stack_depth, engine="warp", codegen="cached", exact_logpdf=False,
+                    schedule="priority", optimize=True, group_trace_cap=1 << 12, return_machine=True)
+    trs = m.group_traces()
+    assert len(trs) == 3
+    useful = sum(s.active * s.prims.get(t.grad, 0) for tr in trs for s in tr.steps)
+    assert useful == m.useful_grads
+    for tr in trs:
+        assert 0 < RM.utilization(tr, {t.grad}) <= 1
+
+
 @pytest.mark.parametrize("codegen", [False, "cached"])
 def test_warp_engine_nuts_refill(codegen):
     """Chains outnumber the resident lanes 3:1 (4 groups of 32, persistent refill from the
