@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
 def test_struct_layouts_match_header():
     assert OP_DTYPE.itemsize == 56 and BLOCK_DTYPE.itemsize == 32 and VAR_DTYPE.itemsize == 24
     assert C.sizeof(_native.Status) == 64
-    assert C.sizeof(_native.MachineOpts) == 32
+    assert C.sizeof(_native.MachineOpts) == 36  # 9 int32 fields (group_trace_cap added in ABI v3)
 
 
 def test_sass_is_sm100a():
