@@ -898,6 +898,9 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
       m->warps_per_cta = wpc;
       m->tc_smem_off = (int)off_of(wpc);
     }
+    if (!m->fp32 && m->stage_target < 0)  // large per-warp scratch (streamed designs): smaller CTAs
+      while (m->warps_per_cta > 1 && (size_t)m->warps_per_cta * m->lf_smem_per_warp * sizeof(double) > (size_t)smem_optin)
+        --m->warps_per_cta;
     const size_t smem = m->fp32 ? (size_t)m->tc_smem_off + (size_t)m->tc_img_bytes
                                 : ((size_t)m->stage_doubles + (size_t)m->warps_per_cta * m->lf_smem_per_warp) * sizeof(double);
     m->smem_bytes = smem;

@@ -761,20 +761,24 @@ __device__ void warp_lr_nt(const DevTarget& tg, bool part, const uint64_t* xp, u
   }
 }
 
-// Large designs (BASELINE config 4: n = 100k points, sx = 80 MB): one warp reading sx
-// fragment by fragment keeps a few hundred bytes in flight and runs at ~1 GB/s. Instead
-// sx streams through a per-warp shared-memory ring: lane 0 issues bulk async copies
-// (cp.async.bulk, the TMA engine; completion counted in bytes on an mbarrier per stage)
-// of kLrChunk contiguous data points each, kLrStages chunks in flight, and every chunk
-// feeds BOTH GEMMs of the m-tile pass straight from shared memory — margins (B = sx^T:
-// thread (g, c) reads point g, coordinate 4ks + c) and G += s sx (B = sx: point 4kk + c,
-// coordinate 8j + g) — so sx is read once per m-tile pass instead of twice in two
-// fragment orders. Per-warp shared memory: the w tile, the ring, the barriers.
-constexpr int kLrStreamMinN = 16384;  // designs at least this tall stream (host: engine.cu)
-constexpr int kLrChunk = 16;          // data points per stage (two 8-point n-tiles)
-constexpr int kLrStages = 3;
+// Logistic regression with the design streamed (every design of at least kLrStreamMinN
+// points, e.g. BASELINE config 3 at 1000 x 25 and config 4 at 100k x 100 = 80 MB): reading
+// sx fragment by fragment from L2 leaves one warp waiting on a load chain per 8 points.
+// Instead sx streams through a per-warp shared-memory ring: lane 0 issues bulk async copies
+// (cp.async.bulk, the TMA engine; completion counted in bytes on an mbarrier per stage) of
+// kLrChunk contiguous data points each, kLrStages - 1 chunks in flight while one is
+// consumed, and every chunk feeds BOTH GEMMs of the m-tile pass straight from shared
+// memory — margins (B = sx^T: thread (g, c) reads point g, coordinate 4ks + c) and
+// G += s sx (B = sx: point 4kk + c, coordinate 8j + g) — so sx is read once per m-tile pass
+// instead of twice in two fragment orders. The chunk's two n-tiles of margins accumulate
+// in four independent DMMA chains (even / odd k-steps), which keeps the DMMA pipe busy
+// instead of waiting out one 25-deep dependent chain at d = 100.
+// Per-warp shared memory: the w tile, the ring, the barriers.
+constexpr int kLrStreamMinN = 512;  // designs at least this tall stream (host: engine.cu)
+constexpr int kLrChunk = 16;        // data points per stage (two 8-point n-tiles)
+constexpr int kLrStages = 4;
 __host__ __device__ __forceinline__ int lr_stream_doubles(int d) {
-  return 8 * lf_stride_q(d) + kLrStages * kLrChunk * d + kLrStages + 1;  // + barriers, even
+  return 8 * lf_stride_q(d) + kLrStages * kLrChunk * d + kLrStages;  // + barriers (even)
 }
 
 template <int NT2, bool LOGPDF>
@@ -794,11 +798,12 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
     lsbtc::fence_barrier_init();
   }
   __syncwarp();
-  auto issue = [&](int it) {  // lane 0: chunk it % nch into stage it % kLrStages
+  // lane 0: chunk it % nch into stage it % kLrStages. The stage's previous contents were
+  // consumed (into registers) by every lane before the __syncwarp that precedes the issue.
+  auto issue = [&](int it) {
     const int ch = it % nch, st = it % kLrStages;
     const int pts = min(kLrChunk, n - ch * kLrChunk);
     const uint32_t bytes = (uint32_t)(pts * d * 8) & ~15u;  // an odd tail word: plain load below
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     lsbtc::mbar_expect_tx(&bars[st], bytes);
     if (bytes) lsbtc::bulk_g2s(ring + (size_t)st * kLrChunk * d, tg.P + (size_t)ch * kLrChunk * d, bytes, &bars[st]);
   };
@@ -828,26 +833,34 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
       const_cast<double*>(X)[last] = __ldg(tg.P + (size_t)p0 * d + last);
     }
     __syncwarp();
+    // margins of the chunk's points 0..15 (two n-tiles) for the m-tile's 8 chains, C layout;
+    // rows past the chunk's points read as zero
+    double acc[2][2][2] = {};  // [n-tile][even / odd k-step][element]
+    {
+      const bool pr0 = g < pts, pr1 = 8 + g < pts;
+      const double* b0 = X + (size_t)g * d + c;
+      const double* b1 = b0 + (size_t)8 * d;
+#pragma unroll 2
+      for (int ks = 0; ks < KS; ks += 2) {
+        const int k = 4 * ks + c, k2 = k + 4;
+        const double a0 = Xs[g * SQ + k], a1 = Xs[g * SQ + k2];  // zero padded to SQ >= 4 KS + 4
+        const bool in0 = k < d, in1 = k2 < d;
+        lsb::dmma(acc[0][0], a0, (pr0 && in0) ? b0[4 * ks] : 0.0);
+        lsb::dmma(acc[1][0], a0, (pr1 && in0) ? b1[4 * ks] : 0.0);
+        lsb::dmma(acc[0][1], a1, (pr0 && in1) ? b0[4 * ks + 4] : 0.0);
+        lsb::dmma(acc[1][1], a1, (pr1 && in1) ? b1[4 * ks + 4] : 0.0);
+      }
+    }
 #pragma unroll
     for (int t = 0; t < kLrChunk / 8; ++t) {
-      if (8 * t >= pts) break;  // warp-uniform
-      // margins of points 8t..8t+7 of the chunk for the m-tile's 8 chains (C layout)
-      double acc[2] = {0.0, 0.0};
-      const bool prow = 8 * t + g < pts;
-      const double* bp = X + (size_t)(8 * t + g) * d + c;
-#pragma unroll 5
-      for (int ks = 0; ks < KS; ++ks) {
-        const int k = 4 * ks + c;
-        lsb::dmma(acc, Xs[g * SQ + k], (prow && k < d) ? bp[4 * ks] : 0.0);
-      }
+      const double m0 = __dadd_rn(acc[t][0][0], acc[t][1][0]), m1 = __dadd_rn(acc[t][0][1], acc[t][1][1]);
       if (LOGPDF) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (8 * t + 2 * c + e < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -acc[e]));
+        if (8 * t + 2 * c < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -m0));
+        if (8 * t + 2 * c + 1 < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -m1));
         continue;
       }
-      const double s0 = 8 * t + 2 * c < pts ? lsb::lr_sig(acc[0]) : 0.0;
-      const double s1 = 8 * t + 2 * c + 1 < pts ? lsb::lr_sig(acc[1]) : 0.0;
+      const double s0 = 8 * t + 2 * c < pts ? lsb::lr_sig(m0) : 0.0;
+      const double s1 = 8 * t + 2 * c + 1 < pts ? lsb::lr_sig(m1) : 0.0;
       const double u0 = __shfl_sync(kFull, s0, q0), u1 = __shfl_sync(kFull, s1, q0);
       const double v0 = __shfl_sync(kFull, s0, q1), v1 = __shfl_sync(kFull, s1, q1);
       const double a0 = hi ? u1 : u0, a1 = hi ? v1 : v0;

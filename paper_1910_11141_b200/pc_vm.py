@@ -206,8 +206,9 @@ class Machine:
                     p[names[0]] = g
             prims.append(p)
         out = []
+        width = min(32, self.z)  # a group's lanes (a batch of <= 32 chains is one group)
         for recs in self._h.group_traces():
-            tr = ScheduleTrace(engine="pc", z=32)
+            tr = ScheduleTrace(engine="pc", z=width)
             for r in recs:
                 b, act = int(r) & 0xffff, int(r) >> 16
                 tr.record(self.labels[b], act, prims[b])
