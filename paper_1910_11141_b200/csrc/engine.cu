@@ -519,6 +519,7 @@ struct ls_machine {
   int lf_smem_per_warp = 0;
   int warps_per_cta = 4;     // warp engine CTA shape
   size_t smem_bytes = 0;     // warp engine dynamic shared memory per CTA
+  int carveout = -1;         // its preferred shared-memory carveout (cudaSharedmemCarveout*)
   int stage_target = -1;     // target whose B fragments each CTA stages in shared memory
   int stage_doubles = 0;
   // fp32 arm (LS_MF_FP32): tensor-core superblocks, warpgroup stepping
@@ -906,6 +907,14 @@ int ls_machine_create(ls_program* p, int64_t z, int32_t depth, const ls_machine_
     m->smem_bytes = smem;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // machines with large per-warp scratch (not the staged-target or fp32 CTAs, which hold
+    // one CTA per SM by design) let the whole unified L1/shared array go to shared
+    // memory: without that preference the occupancy query (and the launch) size the
+    // carveout for one such CTA per SM (measured: 1 CTA of 62.6 KB where 3 fit); the others
+    // keep the default split (L1 for the block code's loads). Set again at every launch.
+    m->carveout = (smem > 48 * 1024 && !m->fp32 && m->stage_target < 0) ? (int)cudaSharedmemCarveoutMaxShared
+                                                                          : (int)cudaSharedmemCarveoutDefault;
+    cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, m->carveout);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vm_warp_kernel, 32 * m->warps_per_cta, smem) !=
             cudaSuccess || per_sm < 1) {
@@ -1100,6 +1109,7 @@ int ls_run(ls_machine* m, int64_t max_steps, ls_status* st) {
     if (m->warp) CK(cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     else CK(cudaFuncSetAttribute(vm_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
+  if (m->warp) CK(cudaFuncSetAttribute(vm_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, m->carveout));
   CK(cudaMemsetAsync(m->flags + 1, 0, 2 * sizeof(int), m->stream));
   if (!m->ev0) {
     CK(cudaEventCreate(&m->ev0));

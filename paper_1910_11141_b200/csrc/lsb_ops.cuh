@@ -182,4 +182,11 @@ __device__ __forceinline__ double lr_sig(double m) {
   return 1.0 / (1.0 + exp(m));
 }
 
+// the same sigmoid(-m) without a divergent branch: exp(-|m|) is the exp both branches of
+// lr_sig take, so every result is bit-identical
+__device__ __forceinline__ double lr_sig_nb(double m) {
+  const double e = exp(-fabs(m));
+  return __ddiv_rn(m >= 0 ? e : 1.0, __dadd_rn(1.0, e));
+}
+
 }  // namespace lsb

@@ -766,29 +766,31 @@ __device__ void warp_lr_nt(const DevTarget& tg, bool part, const uint64_t* xp, u
 // sx fragment by fragment from L2 leaves one warp waiting on a load chain per 8 points.
 // Instead sx streams through a per-warp shared-memory ring: lane 0 issues bulk async copies
 // (cp.async.bulk, the TMA engine; completion counted in bytes on an mbarrier per stage) of
-// kLrChunk contiguous data points each, kLrStages - 1 chunks in flight while one is
-// consumed, and every chunk feeds BOTH GEMMs of the m-tile pass straight from shared
-// memory — margins (B = sx^T: thread (g, c) reads point g, coordinate 4ks + c) and
-// G += s sx (B = sx: point 4kk + c, coordinate 8j + g) — so sx is read once per m-tile pass
-// instead of twice in two fragment orders. The chunk's two n-tiles of margins accumulate
-// in four independent DMMA chains (even / odd k-steps), which keeps the DMMA pipe busy
-// instead of waiting out one 25-deep dependent chain at d = 100.
+// kLrChunk contiguous data points, the next chunk in flight while one is consumed, and every
+// chunk feeds BOTH GEMMs of the m-tile pass straight from shared memory — margins (B = sx^T:
+// thread (g, c) reads point g, coordinate 4ks + c) and G += s sx (B = sx: point 4kk + c,
+// coordinate 8j + g) — so sx is read once per m-tile pass instead of twice in two fragment
+// orders. DMMA results land ~100 cycles after issue, so a chunk's margins accumulate in
+// eight independent chains (four n-tiles x even / odd k-steps) and its 13 gradient
+// accumulators interleave; the sigmoid is branch-free (no divergence between lanes).
 // Per-warp shared memory: the w tile, the ring, the barriers.
 constexpr int kLrStreamMinN = 512;  // designs at least this tall stream (host: engine.cu)
-constexpr int kLrChunk = 16;        // data points per stage (two 8-point n-tiles)
-constexpr int kLrStages = 4;
+constexpr int kLrChunk = 32;        // data points per stage (four 8-point n-tiles)
+constexpr int kLrStages = 2;        // one chunk in flight while one is consumed (copy << compute)
+constexpr int kLrNt = kLrChunk / 8;
 __host__ __device__ __forceinline__ int lr_stream_doubles(int d) {
   return 8 * lf_stride_q(d) + kLrStages * kLrChunk * d + kLrStages;  // + barriers (even)
 }
 
 template <int NT2, bool LOGPDF>
-__device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+__device__ __noinline__ void warp_lr_stream(const DevTarget& tgr, bool part, const uint64_t* xp, uint64_t* dst,
                                             double* sm) {
   const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n_act = __popc(mask);
   if (n_act == 0) return;
-  const int d = tg.dim, n = tg.n, SQ = lf_stride_q(d), KS = (d + 3) / 4;
+  const int d = tgr.dim, n = tgr.n, SQ = lf_stride_q(d), KS = (d + 3) / 4;
+  const double* const sx = tgr.P;
   double* Xs = sm;
   double* ring = sm + 8 * SQ;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kLrStages * kLrChunk * d);
@@ -798,24 +800,31 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
     lsbtc::fence_barrier_init();
   }
   __syncwarp();
-  // lane 0: chunk it % nch into stage it % kLrStages. The stage's previous contents were
-  // consumed (into registers) by every lane before the __syncwarp that precedes the issue.
-  auto issue = [&](int it) {
-    const int ch = it % nch, st = it % kLrStages;
+  // lane 0: chunk ch into stage st. The stage's previous contents were consumed (into
+  // registers) by every lane before the __syncwarp that precedes the issue.
+  auto issue = [&](int ch, int st) {
     const int pts = min(kLrChunk, n - ch * kLrChunk);
     const uint32_t bytes = (uint32_t)(pts * d * 8) & ~15u;  // an odd tail word: plain load below
     lsbtc::mbar_expect_tx(&bars[st], bytes);
-    if (bytes) lsbtc::bulk_g2s(ring + (size_t)st * kLrChunk * d, tg.P + (size_t)ch * kLrChunk * d, bytes, &bars[st]);
+    if (bytes) lsbtc::bulk_g2s(ring + (size_t)st * kLrChunk * d, sx + (size_t)ch * kLrChunk * d, bytes, &bars[st]);
   };
+  // the item sequence (m-tile pass mt, chunk ch) is walked twice: issue runs kLrStages ahead
+  int ich = 0, ist = 0;
+  const int pre = min(kLrStages, total);
   if (lane == 0)
-    for (int it = 0; it < min(kLrStages, total); ++it) issue(it);
+    for (int i = 0; i < pre; ++i) {
+      issue(ich, ist);
+      if (++ich == nch) ich = 0;
+      if (++ist == kLrStages) ist = 0;
+    }
   const int q0 = (lane & ~3) | (c >> 1), q1 = q0 + 2;
   const bool hi = (lane & 1) != 0;
   double G[NT2][2];
   double lp = 0.0;
   int src = -1;
+  int mt = 0, ch = 0, st = 0;
+  uint32_t par = 0;
   for (int it = 0; it < total; ++it) {
-    const int mt = it / nch, ch = it % nch, st = it % kLrStages;
     if (ch == 0) {  // a new m-tile pass: stage its 8 chains' w, clear the accumulators
       src = mtile_lane(mask, n_act, mt, g);
       __syncwarp();
@@ -827,40 +836,41 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
     }
     const int p0 = ch * kLrChunk, pts = min(kLrChunk, n - p0);
     const double* X = ring + (size_t)st * kLrChunk * d;
-    lsbtc::mbar_wait(&bars[st], (uint32_t)((it / kLrStages) & 1));
+    lsbtc::mbar_wait(&bars[st], par);
     if (((pts * d) & 1) && lane == 0) {
       const size_t last = (size_t)pts * d - 1;
-      const_cast<double*>(X)[last] = __ldg(tg.P + (size_t)p0 * d + last);
+      const_cast<double*>(X)[last] = __ldg(sx + (size_t)p0 * d + last);
     }
     __syncwarp();
-    // margins of the chunk's points 0..15 (two n-tiles) for the m-tile's 8 chains, C layout;
-    // rows past the chunk's points read as zero
-    double acc[2][2][2] = {};  // [n-tile][even / odd k-step][element]
+    // margins of the chunk's 32 points (four n-tiles) for the m-tile's 8 chains, C layout,
+    // as eight independent DMMA chains (n-tile x even / odd k-step); rows past the chunk's
+    // points read as zero
+    double acc[kLrNt][2][2] = {};
     {
-      const bool pr0 = g < pts, pr1 = 8 + g < pts;
       const double* b0 = X + (size_t)g * d + c;
-      const double* b1 = b0 + (size_t)8 * d;
 #pragma unroll 2
       for (int ks = 0; ks < KS; ks += 2) {
         const int k = 4 * ks + c, k2 = k + 4;
         const double a0 = Xs[g * SQ + k], a1 = Xs[g * SQ + k2];  // zero padded to SQ >= 4 KS + 4
         const bool in0 = k < d, in1 = k2 < d;
-        lsb::dmma(acc[0][0], a0, (pr0 && in0) ? b0[4 * ks] : 0.0);
-        lsb::dmma(acc[1][0], a0, (pr1 && in0) ? b1[4 * ks] : 0.0);
-        lsb::dmma(acc[0][1], a1, (pr0 && in1) ? b0[4 * ks + 4] : 0.0);
-        lsb::dmma(acc[1][1], a1, (pr1 && in1) ? b1[4 * ks + 4] : 0.0);
+#pragma unroll
+        for (int t = 0; t < kLrNt; ++t) {
+          const bool pr = 8 * t + g < pts;
+          lsb::dmma(acc[t][0], a0, (pr && in0) ? b0[(size_t)8 * t * d + 4 * ks] : 0.0);
+          lsb::dmma(acc[t][1], a1, (pr && in1) ? b0[(size_t)8 * t * d + 4 * ks + 4] : 0.0);
+        }
       }
     }
 #pragma unroll
-    for (int t = 0; t < kLrChunk / 8; ++t) {
+    for (int t = 0; t < kLrNt; ++t) {
       const double m0 = __dadd_rn(acc[t][0][0], acc[t][1][0]), m1 = __dadd_rn(acc[t][0][1], acc[t][1][1]);
       if (LOGPDF) {
         if (8 * t + 2 * c < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -m0));
         if (8 * t + 2 * c + 1 < pts) lp = __dadd_rn(lp, lsb::np_logaddexp(0.0, -m1));
         continue;
       }
-      const double s0 = 8 * t + 2 * c < pts ? lsb::lr_sig(m0) : 0.0;
-      const double s1 = 8 * t + 2 * c + 1 < pts ? lsb::lr_sig(m1) : 0.0;
+      const double s0 = 8 * t + 2 * c < pts ? lsb::lr_sig_nb(m0) : 0.0;
+      const double s1 = 8 * t + 2 * c + 1 < pts ? lsb::lr_sig_nb(m1) : 0.0;
       const double u0 = __shfl_sync(kFull, s0, q0), u1 = __shfl_sync(kFull, s1, q0);
       const double v0 = __shfl_sync(kFull, s0, q1), v1 = __shfl_sync(kFull, s1, q1);
       const double a0 = hi ? u1 : u0, a1 = hi ? v1 : v0;
@@ -875,7 +885,11 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
       }
     }
     __syncwarp();  // every lane is done with the stage before it is refilled
-    if (lane == 0 && it + kLrStages < total) issue(it + kLrStages);
+    if (lane == 0 && it + kLrStages < total) {
+      issue(ich, ist);
+      if (++ich == nch) ich = 0;
+      if (++ist == kLrStages) ist = 0;
+    }
     if (ch == nch - 1) {  // the m-tile pass is complete
       uint64_t* dg = (uint64_t*)__shfl_sync(kFull, (unsigned long long)dst, src < 0 ? 0 : src);
       if (LOGPDF) {
@@ -894,6 +908,14 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
             if (col < d) dg[(size_t)col * 32] = f64_bits(__dsub_rn(G[j][e], Xs[g * SQ + col]));
           }
       }
+    }
+    if (++st == kLrStages) {
+      st = 0;
+      par ^= 1u;
+    }
+    if (++ch == nch) {
+      ch = 0;
+      ++mt;
     }
   }
   __syncwarp();
