@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--chains", type=int, default=1 << 16, help="chains per GPU")
-    ap.add_argument("--config4-chains", type=int, default=1 << 12, help="config-4 line: chains")
+    ap.add_argument("--config4-chains", type=int, default=1 << 13, help="config-4 line: chains")
     ap.add_argument("--config5-chains", type=int, default=1 << 16, help="config-5 line: chains")
     ap.add_argument("--dim", type=int, default=100)
     ap.add_argument("--iterations", type=int, default=10)

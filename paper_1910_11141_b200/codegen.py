@@ -449,8 +449,17 @@ class _Gen:
         if self.dp.targets[int(op["imm0"])].kind == 2:  # logistic regression: fused DMMA pass
             t = int(op["imm0"])
             cond = f"!a.exact_logpdf && lr_coop(a, a.targets[{t}])" if want_lp else f"lr_coop(a, a.targets[{t}])"
-            lines.append(f"  if ({cond}) {{ __syncwarp(); warp_lr(a.targets[{t}], part_, "
-                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm, {'true' if want_lp else 'false'}, a.lf_smem_per_warp); "
+            nt2 = (int(self.dp.targets[t].dim) + 7) // 8
+            lp_ = 'true' if want_lp else 'false'
+            if nt2 <= 16:  # the streamed body inlined for this target's NT2 (no call-boundary spills)
+                lines.append(f"  if ({cond} && lr_streams(a.targets[{t}], a.lf_smem_per_warp)) {{ __syncwarp(); "
+                             f"warp_lr_stream_body<{nt2}, {lp_}>(a.targets[{t}], part_, "
+                             f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm); __syncwarp(); }}")
+                cond = "else if (" + cond + ")"
+            else:
+                cond = "if (" + cond + ")"
+            lines.append(f"  {cond} {{ __syncwarp(); warp_lr(a.targets[{t}], part_, "
+                         f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm, {lp_}, a.lf_smem_per_warp); "
                          "__syncwarp(); }")
             if want_lp:
                 lines.append(f"  else if (part_) cd_[0] = f64_bits(target_logpdf(a.targets[{t}], {x}, S, 1));")

@@ -782,9 +782,18 @@ __host__ __device__ __forceinline__ int lr_stream_doubles(int d) {
   return 8 * lf_stride_q(d) + kLrStages * kLrChunk * d + kLrStages;  // + barriers (even)
 }
 
+// The body is force-inlined where the program-specialised code calls it for its target's
+// NT2 (measured: as an out-of-line call inside the VM kernel the G accumulators spill and a
+// chunk takes twice as long as the same code compiled on its own); the interpreter calls
+// the out-of-line warp_lr_stream below.
+#ifdef LSB_GENERATED
+#define LSB_LRS_QUAL __forceinline__
+#else
+#define LSB_LRS_QUAL __noinline__
+#endif
 template <int NT2, bool LOGPDF>
-__device__ __noinline__ void warp_lr_stream(const DevTarget& tgr, bool part, const uint64_t* xp, uint64_t* dst,
-                                            double* sm) {
+__device__ LSB_LRS_QUAL void warp_lr_stream_body(const DevTarget& tgr, bool part, const uint64_t* xp,
+                                                    uint64_t* dst, double* sm) {
   const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n_act = __popc(mask);
@@ -925,11 +934,27 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tgr, bool part, con
   __syncwarp();
 }
 
+#ifdef LSB_GENERATED
+template <int NT2, bool LOGPDF>
+__device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst,
+                                            double* sm) {
+  warp_lr_stream_body<NT2, LOGPDF>(tg, part, xp, dst, sm);
+}
+#else  // the interpreter library: the body itself is the out-of-line function (a wrapper
+       // around a force-inlined body made ptxas run for hours on the interpreter kernel)
+#define warp_lr_stream warp_lr_stream_body
+#endif
+
+// does this machine stream target tg's design (warp_lr dispatch; codegen emits the same test)
+__device__ __forceinline__ bool lr_streams(const DevTarget& tg, int sm_doubles) {
+  return tg.n >= kLrStreamMinN && sm_doubles >= lr_stream_doubles(tg.dim);
+}
+
 // grad (want_logpdf = false) or fast logpdf of a logistic-regression target, DMMA path;
 // sm_doubles: the warp's shared-memory scratch (tall designs stream through it)
 __device__ inline void warp_lr(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst, double* Xs,
                                bool want_logpdf, int sm_doubles) {
-  if (tg.n >= kLrStreamMinN && sm_doubles >= lr_stream_doubles(tg.dim)) {
+  if (lr_streams(tg, sm_doubles)) {
     switch (tg.NT2) {
 #define LSB_LRS_CASE(K)                                                        \
   case K:                                                                      \
