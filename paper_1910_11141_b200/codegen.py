@@ -451,7 +451,10 @@ class _Gen:
             cond = f"!a.exact_logpdf && lr_coop(a, a.targets[{t}])" if want_lp else f"lr_coop(a, a.targets[{t}])"
             nt2 = (int(self.dp.targets[t].dim) + 7) // 8
             lp_ = 'true' if want_lp else 'false'
-            if nt2 <= 16:  # the streamed body inlined for this target's NT2 (no call-boundary spills)
+            # wide designs (NT2 >= 8): the streamed body inlined for this target's NT2 — as an
+            # out-of-line call its 2·NT2 accumulators spill (config 4: 1.7x faster inlined);
+            # narrow ones keep the call (config 3 at NT2 = 4 measured 2x slower inlined)
+            if 8 <= nt2 <= 16:
                 lines.append(f"  if ({cond} && lr_streams(a.targets[{t}], a.lf_smem_per_warp)) {{ __syncwarp(); "
                              f"warp_lr_stream_body<{nt2}, {lp_}>(a.targets[{t}], part_, "
                              f"part_ ? (const uint64_t*){x} : nullptr, cd_, sm); __syncwarp(); }}")
