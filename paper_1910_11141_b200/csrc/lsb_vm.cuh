@@ -787,13 +787,16 @@ __host__ __device__ __forceinline__ int lr_stream_doubles(int d) {
 // chunk takes twice as long as the same code compiled on its own); the interpreter calls
 // the out-of-line warp_lr_stream below.
 #ifdef LSB_GENERATED
+#define LSB_LRS_NAME warp_lr_stream_body
 #define LSB_LRS_QUAL __forceinline__
-#else
+#else  // the interpreter library: the body itself is the out-of-line warp_lr_stream (the same
+       // text as a wrapper around a force-inlined body made ptxas run for over an hour)
+#define LSB_LRS_NAME warp_lr_stream
 #define LSB_LRS_QUAL __noinline__
 #endif
 template <int NT2, bool LOGPDF>
-__device__ LSB_LRS_QUAL void warp_lr_stream_body(const DevTarget& tgr, bool part, const uint64_t* xp,
-                                                    uint64_t* dst, double* sm) {
+__device__ LSB_LRS_QUAL void LSB_LRS_NAME(const DevTarget& tgr, bool part, const uint64_t* xp, uint64_t* dst,
+                                          double* sm) {
   const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
   const unsigned mask = __ballot_sync(kFull, part);
   const int n_act = __popc(mask);
@@ -940,9 +943,6 @@ __device__ __noinline__ void warp_lr_stream(const DevTarget& tg, bool part, cons
                                             double* sm) {
   warp_lr_stream_body<NT2, LOGPDF>(tg, part, xp, dst, sm);
 }
-#else  // the interpreter library: the body itself is the out-of-line function (a wrapper
-       // around a force-inlined body made ptxas run for hours on the interpreter kernel)
-#define warp_lr_stream warp_lr_stream_body
 #endif
 
 // does this machine stream target tg's design (warp_lr dispatch; codegen emits the same test)
@@ -954,7 +954,7 @@ __device__ __forceinline__ bool lr_streams(const DevTarget& tg, int sm_doubles) 
 // sm_doubles: the warp's shared-memory scratch (tall designs stream through it)
 __device__ inline void warp_lr(const DevTarget& tg, bool part, const uint64_t* xp, uint64_t* dst, double* Xs,
                                bool want_logpdf, int sm_doubles) {
-  if (lr_streams(tg, sm_doubles)) {
+  if (tg.n >= kLrStreamMinN && sm_doubles >= lr_stream_doubles(tg.dim)) {  // = lr_streams
     switch (tg.NT2) {
 #define LSB_LRS_CASE(K)                                                        \
   case K:                                                                      \
