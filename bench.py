@@ -264,7 +264,7 @@ def host_info() -> dict:
             "blas": blas, "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
 
 
-def cpu_baseline(args, cfg, target, cp, reps: int = 3) -> tuple[dict, np.ndarray]:
+def cpu_baseline(args, cfg, target, cp, reps: int = 5) -> tuple[dict, np.ndarray]:
     """Warm best-of-`reps` of the pc engine port plus one run_local, both on the same
     bounded sample (chains 0..cpu_chains-1 of the workload, cpu_iterations iterations)."""
     cpu_reference_sample(args, cfg, target, cp, 16, 2)  # warm: imports, numpy dispatch
