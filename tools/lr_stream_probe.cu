@@ -1,7 +1,8 @@
 // warp_lr_stream in isolation, with parts switched off (V bits: 1 no sigmoid, 2 no G GEMM,
-// 4 no margin GEMM) (dev tool). lrs_v is a snapshot of warp_lr_stream_body (csrc/lsb_vm.cuh)
-// with those switches added; re-take it after changing the kernel.: one warp per CTA, one gradient call over a tall
-// design, timed with CUDA events — separates the kernel's own speed from the VM context.
+// 4 no margin GEMM) (dev tool): one warp per CTA, one gradient call over a tall design, timed
+// with CUDA events — separates the kernel's own speed from the VM context. lrs_v is a
+// snapshot of warp_lr_stream_body (csrc/lsb_vm.cuh) with those switches added; re-take it
+// after changing the kernel.
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -I include \
 //        -o lr_stream_probe tools/lr_stream_probe.cu
 #include <cstdio>
